@@ -1,0 +1,171 @@
+/*
+ * detgpu — C-ABI of the B200-native deterministic inference engine.
+ *
+ * This is the drop-in boundary for the reference's deterministic compute core
+ * (reference proj/include/verinf/detcore.hpp:151-163, proj/src/detcore.cpp:380-410) and the
+ * receipt output hash (proj/src/receipts.cpp:119-120). Plain pointers and sizes only; no torch or
+ * C++ types cross it. Callers own every buffer. All functions are thread-safe across handles;
+ * calls on one handle are serialised by the caller (one handle per GPU = one replica).
+ *
+ * Errors: functions return DETGPU_OK or a DETGPU_E* code; detgpu_last_error(h) (or
+ * detgpu_global_error() when no handle exists) gives the diagnostic. DETGPU_EINVAL is the
+ * counterpart of the reference's std::invalid_argument (unknown arch, malformed policy,
+ * out-of-vocabulary prompt token, batch_size == 0, non-finite values).
+ */
+#ifndef DETGPU_H
+#define DETGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DETGPU_OK 0
+#define DETGPU_EINVAL 1      /* std::invalid_argument in the reference */
+#define DETGPU_ECUDA 2       /* CUDA runtime / launch failure */
+#define DETGPU_ENOMEM 3      /* device or host allocation failed */
+#define DETGPU_ENONFINITE 4  /* non-finite logits (reference check_finite, detcore.cpp:127-133) */
+#define DETGPU_ENODEV 5      /* no sm_100 device */
+
+/* DecodeKind (detcore.hpp:50). */
+#define DETGPU_GREEDY 0
+#define DETGPU_TOP_K 1
+#define DETGPU_NUCLEUS 2
+
+/* DecodePolicy (detcore.hpp:52-66): k present iff top_k, p present iff nucleus. */
+typedef struct detgpu_policy {
+    uint8_t kind;
+    uint8_t has_k;
+    uint8_t has_p;
+    uint8_t reserved;
+    uint32_t k;
+    float p;
+    uint32_t max_tokens;
+} detgpu_policy;
+
+typedef struct detgpu_model_info {
+    uint32_t n_layers;
+    uint32_t d_model;
+    uint32_t n_heads;
+    uint32_t n_kv_heads;
+    uint32_t head_dim;
+    uint32_t ffn;
+    uint32_t vocab;
+    uint32_t toy; /* 1: the reference ToyModel (detcore.hpp:139-149) run on the GPU */
+    float rope_theta;
+    float rms_eps;
+    uint64_t n_params;
+    uint64_t weight_bytes;
+} detgpu_model_info;
+
+/* Per-call device timings (CUDA events on the engine stream) and byte counts. */
+typedef struct detgpu_stats {
+    float prefill_ms;
+    float decode_ms;       /* decode loop: steps 1..T-1 forward + all sampling */
+    float d2h_ms;          /* device->host copies of tokens and logits */
+    float hash_ms;         /* host SHA-256 of canonical bytes (wall) */
+    uint64_t decode_steps; /* forward passes in the decode loop */
+    uint64_t tokens;       /* generated tokens (sum over requests) */
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t kernel_launches;
+} detgpu_stats;
+
+/* Flags for detgpu_generate. */
+#define DETGPU_F_DEVICE_ONLY 1u /* keep tokens/logits in HBM: no D2H, no out_hash (bench `value`) */
+
+typedef struct detgpu_engine detgpu_engine;
+
+const char* detgpu_version(void);
+const char* detgpu_global_error(void);
+
+/* Approved architecture profiles (ArchRegistry::defaults, detcore.cpp:12-20, plus "b200"). */
+int detgpu_arch_supported(const char* arch);
+
+/*
+ * Create an engine on `device` for `model_id` under `arch`:
+ *   arch "archA" / "archB": the reference ToyModel with that accumulation profile, any model_id
+ *                           (weights from fnv1a64(model_id), detcore.cpp:275-296);
+ *   arch "b200": a Llama-style transformer whose shape is named by the model_id prefix
+ *                ("llama-tiny" | "llama3-8b"), weights counter-generated from fnv1a64(model_id).
+ * max_batch: requests decoded together (1..256); max_context: prompt + generated tokens.
+ * Replaces ToyModel::from_model_id + ArchRegistry::find (detcore.cpp:288, 333).
+ */
+int detgpu_create(int device, const char* model_id, const char* arch, uint32_t max_batch,
+                  uint32_t max_context, detgpu_engine** out);
+void detgpu_destroy(detgpu_engine* h);
+int detgpu_get_model_info(const detgpu_engine* h, detgpu_model_info* out);
+const char* detgpu_last_error(const detgpu_engine* h);
+
+/*
+ * Run n_req requests (reference infer_batch, detcore.cpp:387-410; infer == n_req 1).
+ * Requests are decoded in groups of at most batch_size (0 -> DETGPU_EINVAL, detcore.cpp:389);
+ * the bytes of each request do not depend on the grouping.
+ *   prompts[i][0..prompt_lens[i]) token ids; seeds[i] seeds the request's xoshiro256++ stream.
+ *   tokens_out[i]  : policies[i].max_tokens u32 (may be NULL with DETGPU_F_DEVICE_ONLY)
+ *   logits_out     : NULL, or an array of n_req pointers each NULL or max_tokens*vocab f32
+ *   out_hash       : NULL or n_req*32 bytes: SHA-256 of the canonical output bytes
+ *                    (detcore.cpp:73-84 layout, receipts.cpp:120 commitment)
+ *   stats          : NULL or filled with timings
+ */
+int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* prompts,
+                    const uint32_t* prompt_lens, const detgpu_policy* policies, const uint64_t* seeds,
+                    uint32_t batch_size, uint32_t* const* tokens_out, float* const* logits_out,
+                    uint8_t* out_hash, uint32_t flags, detgpu_stats* stats);
+
+/* ---- host-side helpers of the receipt path (no GPU needed) ---- */
+
+/* SHA-256 (receipts.hpp:53-54 hash_commit; sha256.cpp:32-37). */
+void detgpu_sha256(const uint8_t* data, size_t n, uint8_t out[32]);
+/* Canonical output size and encoding (detcore.cpp:73-84). */
+size_t detgpu_canonical_size(uint32_t n_tokens, uint32_t vocab);
+void detgpu_encode_canonical(const uint32_t* tokens, uint32_t n_tokens, const float* logits,
+                             uint32_t vocab, uint8_t* out);
+/* SHA-256 of the canonical bytes without materialising them. */
+void detgpu_hash_canonical(const uint32_t* tokens, uint32_t n_tokens, const float* logits,
+                           uint32_t vocab, uint8_t out[32]);
+/* ExecutionTuple encoding (codec.cpp:67-104, big-endian, length-prefixed); returns the size,
+ * writes when out != NULL. req_hash = SHA-256 of these bytes (receipts.cpp:119). */
+size_t detgpu_encode_exec_tuple(const char* model_id, const uint8_t container_digest[32], const char* arch,
+                                const char* driver_tag, const detgpu_policy* policy, uint64_t seed,
+                                const uint32_t* prompt, uint32_t prompt_len, uint8_t* out);
+/* Strict decoder (rejects has_k/has_p outside {0,1}, payload on absent fields and trailing
+ * bytes — the reference decoder's malleability, codec.cpp:76-91, is not inherited).
+ * Returns DETGPU_OK and fills the outputs, or DETGPU_EINVAL. String outputs are NUL-terminated
+ * into caller buffers of *_cap bytes; prompt_out has prompt_cap entries. */
+int detgpu_decode_exec_tuple(const uint8_t* bytes, size_t n, char* model_id, size_t model_id_cap,
+                             uint8_t container_digest[32], char* arch, size_t arch_cap, char* driver_tag,
+                             size_t driver_cap, detgpu_policy* policy, uint64_t* seed, uint32_t* prompt_out,
+                             uint32_t prompt_cap, uint32_t* prompt_len);
+
+/* ---- kernel-level entry points (device pointers; used by the parity tests and the bench) ---- */
+
+/* Y[col*ldy + n] = sum_k X[col*K + k] * W[n*K + k]; W [n_out,K] bf16, X [ncols,K] bf16. */
+int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy,
+                  void* stream);
+/* out[col][i] = bf16(x[col][i] * rstd * gamma[i]); x f32 [ncols,d]; canonical-tree sum of squares. */
+int detgpu_k_rmsnorm(const float* x, const void* gamma, void* out, int ncols, int d, float eps, void* stream);
+/* f32 exp of n values with the engine's det_expf. */
+int detgpu_k_expf(const float* x, float* y, int64_t n, void* stream);
+/* Canonical tree sum of each of `rows` rows of length n (f32) -> out[rows]. */
+int detgpu_k_tree_sum(const float* x, float* out, int rows, int n, void* stream);
+/* Deterministic weight generation of one logical tensor into bf16. */
+int detgpu_k_init_tensor(void* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp, int is_gamma,
+                         int row_mul, int row_add, void* stream);
+/* Softmax + decode step on f32 logits rows (device). probs_out may be NULL. prng_state [rows][4]
+ * is advanced once per row. tokens_out [rows]. Policies host array of `rows`. */
+int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_policy* policies, uint64_t* prng_state,
+                    uint32_t* tokens_out, float* probs_out, int32_t* status_out, void* stream);
+/* Decode attention for `ncols` queries against a contiguous (non-paged) cache:
+ *   q [ncols][hq*hd] bf16, k/v [ncols? no: per query col] -> see tests/test_gpu_kernels.py. */
+int detgpu_k_attention(const void* q, const void* kcache, const void* vcache, const int32_t* block_table,
+                       const int32_t* col_pos, const int32_t* col_req, void* out, int ncols, int hq, int hkv,
+                       int hd, int page, int max_pages, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DETGPU_H */

@@ -1,0 +1,936 @@
+// =====================================================================================
+//  CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+//  A plain C++ restatement of the reference's deterministic inference path, used by tests/,
+//  __graft_entry__.smoke() and bench.py's cpu_baseline leg as the CHECKER. Nothing in the
+//  product (paper_2602_00182_b200/) links, loads or calls this file.
+//
+//  Parity anchors (reference = /root/reference/proj, read-only):
+//    prng ............ include/verinf/prng.hpp:18-87
+//    fnv1a64 ......... src/detcore.cpp:266-273
+//    tree / seq sum .. src/detcore.cpp:135-163
+//    det_matvec ...... src/detcore.cpp:165-185
+//    det_softmax ..... src/detcore.cpp:187-198   (std::exp == glibc expf, restated below)
+//    decode rules .... src/detcore.cpp:202-262
+//    ToyModel ........ src/detcore.cpp:275-315, run loop :319-410
+//    canonical bytes . src/detcore.cpp:73-84
+//    exec tuple ...... src/codec.cpp:67-104 ; SHA-256: FIPS 180-4 (reference: libsodium)
+//  Pinned by: tests/golden/toy_reference.json (outputs of the reference itself, compiled by
+//  oracle/Makefile `ref` into oracle/_ref/), the reference's own KATs (test_detcore.cpp:38-50,
+//  79-89, 153-237; test_receipts.cpp:36-41) and oracle/check_expf.c (exhaustive expf pin).
+//
+//  The Llama-style transformer below has NO counterpart in the reference: its
+//  parity is "unpinned" against the reference and defined by DESIGN.md §3, which it restates with
+//  the reference's conventions (tree sums, no contraction, f32 RNE, bf16 RNE storage).
+// =====================================================================================
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace orc {
+
+// ---------------------------------------------------------------- PRNG (prng.hpp)
+static inline uint64_t splitmix64(uint64_t& x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static inline uint64_t mix_seed(uint64_t a, uint64_t b) {
+    uint64_t x = a ^ (0x9E3779B97F4A7C15ULL + (b << 6) + (b >> 2));
+    uint64_t s = x;
+    return splitmix64(s);
+}
+static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+struct Prng {
+    uint64_t s[4] = {1, 2, 3, 4};
+    static Prng seeded(uint64_t seed) {
+        Prng p;
+        uint64_t x = seed;
+        for (auto& w : p.s) w = splitmix64(x);
+        if ((p.s[0] | p.s[1] | p.s[2] | p.s[3]) == 0) p.s[0] = 0x9E3779B97F4A7C15ULL;
+        return p;
+    }
+    uint64_t next_u64() {
+        const uint64_t result = rotl(s[0] + s[3], 23) + s[0];
+        const uint64_t t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = rotl(s[3], 45);
+        return result;
+    }
+    float next_unit_f32() { return float(next_u64() >> 40) * 0x1.0p-24f; }
+    float next_symmetric_f32() { return float(next_u64() >> 40) * 0x1.0p-23f - 1.0f; }
+    uint64_t next_below(uint64_t bound) {
+        const uint64_t limit = bound * ((~uint64_t{0}) / bound);
+        for (;;) {
+            uint64_t x = next_u64();
+            if (x < limit) return x % bound;
+        }
+    }
+};
+
+static uint64_t fnv1a64(const char* s) {
+    uint64_t h = 0xCBF29CE484222325ULL;
+    for (const unsigned char* c = reinterpret_cast<const unsigned char*>(s); *c; ++c) {
+        h ^= *c;
+        h *= 0x100000001B3ULL;
+    }
+    return h;
+}
+
+// ---------------------------------------------------------------- reductions (detcore.cpp:135-157)
+static float tree_reduce(const float* values, size_t n) {
+    if (n == 0) return 0.0f;
+    thread_local std::vector<float> level;
+    level.assign(values, values + n);
+    while (n > 1) {
+        size_t half = n / 2;
+        for (size_t i = 0; i < half; ++i) level[i] = level[2 * i] + level[2 * i + 1];
+        if (n % 2 != 0) {
+            level[half] = level[n - 1];
+            n = half + 1;
+        } else {
+            n = half;
+        }
+    }
+    return level[0];
+}
+static float sequential_reduce(const float* v, size_t n) {
+    if (n == 0) return 0.0f;
+    float acc = v[0];
+    for (size_t i = 1; i < n; ++i) acc += v[i];
+    return acc;
+}
+static bool all_finite(const float* v, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(v[i])) return false;
+    return true;
+}
+
+// ---------------------------------------------------------------- expf
+// glibc 2.39 x86-64 expf (FMA variant, which the reference's std::exp resolves to on this image):
+// k = round(x*32/ln2), 2^(k/32) from a table, cubic correction, binary64 with fused multiply-adds.
+// The table is computed here from exp2l (not copied); check_expf.c pins this function against
+// libm for every float in [-104, 88.72].
+static uint64_t g_tab[32];
+static bool init_tab() {
+    for (int i = 0; i < 32; ++i) {
+        double d = static_cast<double>(exp2l(static_cast<long double>(i) / 32.0L));
+        uint64_t u;
+        std::memcpy(&u, &d, 8);
+        g_tab[i] = u - (static_cast<uint64_t>(i) << 47);
+    }
+    return true;
+}
+static const bool g_tab_ready = init_tab();
+
+static float det_expf(float x) {
+    uint32_t ux;
+    std::memcpy(&ux, &x, 4);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    if (abstop >= 0x42b) {
+        if (ux == 0xff800000u) return 0.0f;
+        if (abstop >= 0x7f8) return x + x;
+        if (x > 0x1.62e42ep6f) return INFINITY;
+        if (x < -0x1.9fe368p6f) return 0.0f;
+    }
+    const double InvLn2N = 0x1.71547652b82fep+0 * 32.0;
+    const double Shift = 0x1.8p+52;
+    const double C0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+    const double C1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+    const double C2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+    const double xd = x;
+    double kd = std::fma(InvLn2N, xd, Shift);
+    uint64_t ki;
+    std::memcpy(&ki, &kd, 8);
+    kd -= Shift;
+    const double r = std::fma(InvLn2N, xd, -kd);
+    uint64_t t = g_tab[ki % 32];
+    t += ki << 47;
+    double s;
+    std::memcpy(&s, &t, 8);
+    const double z = std::fma(C0, r, C1);
+    const double r2 = r * r;
+    double y = std::fma(C2, r, 1.0);
+    y = std::fma(z, r2, y);
+    y = y * s;
+    return static_cast<float>(y);
+}
+
+// ---------------------------------------------------------------- softmax / decode
+// det_softmax (detcore.cpp:187-198). Returns false on empty / non-finite input.
+static bool det_softmax(const float* logits, size_t n, float* out) {
+    if (n == 0 || !all_finite(logits, n)) return false;
+    float maxv = logits[0];
+    for (size_t i = 0; i < n; ++i) maxv = std::max(maxv, logits[i]);
+    std::vector<float> exps(n);
+    for (size_t i = 0; i < n; ++i) exps[i] = det_expf(logits[i] - maxv);
+    const float sum = tree_reduce(exps.data(), n);
+    for (size_t i = 0; i < n; ++i) out[i] = exps[i] / sum;
+    return true;
+}
+
+enum Kind { GREEDY = 0, TOP_K = 1, NUCLEUS = 2 };
+struct Policy {
+    int kind = GREEDY;
+    bool has_k = false;
+    uint32_t k = 0;
+    bool has_p = false;
+    float p = 0.0f;
+    uint32_t max_tokens = 0;
+    // DecodePolicy::validate (detcore.cpp:52-69)
+    bool valid() const {
+        switch (kind) {
+            case GREEDY: return !has_k && !has_p;
+            case TOP_K: return has_k && k != 0 && !has_p;
+            case NUCLEUS: return has_p && (p > 0.0f) && p <= 1.0f && !has_k;
+            default: return false;
+        }
+    }
+};
+
+// decode_with_draw (detcore.cpp:210-254). Returns -1 on the reference's invalid_argument paths.
+static int64_t decode_with_draw(const float* probs, size_t n, const Policy& pol, float r) {
+    if (n == 0 || !all_finite(probs, n)) return -1;
+    for (size_t i = 0; i < n; ++i)
+        if (probs[i] < 0.0f) return -1;
+    if (!pol.valid()) return -1;
+    if (pol.kind == GREEDY) {
+        uint32_t best = 0;
+        for (uint32_t i = 1; i < n; ++i)
+            if (probs[i] > probs[best]) best = i;
+        return best;
+    }
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+        if (probs[a] != probs[b]) return probs[a] > probs[b];
+        return a < b;
+    });
+    size_t kept = n;
+    if (pol.kind == TOP_K) {
+        kept = std::min<size_t>(pol.k, n);
+    } else {
+        float cum = 0.0f;
+        kept = n;
+        for (size_t i = 0; i < n; ++i) {
+            cum += probs[order[i]];
+            if (cum >= pol.p) {
+                kept = i + 1;
+                break;
+            }
+        }
+    }
+    std::vector<float> kp(kept);
+    for (size_t i = 0; i < kept; ++i) kp[i] = probs[order[i]];
+    const float mass = tree_reduce(kp.data(), kept);
+    if (!(mass > 0.0f)) return -1;
+    float cum = 0.0f;
+    for (size_t i = 0; i < kept; ++i) {
+        cum += kp[i] / mass;
+        if (cum >= r) return order[i];
+    }
+    return order[kept - 1];
+}
+
+// ---------------------------------------------------------------- SHA-256 (FIPS 180-4)
+struct Sha256 {
+    uint32_t h[8];
+    uint8_t buf[64];
+    uint64_t total = 0;
+    size_t fill = 0;
+    Sha256() {
+        static const uint32_t iv[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                                       0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+        std::memcpy(h, iv, sizeof(h));
+    }
+    static uint32_t ror(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+    void block(const uint8_t* p) {
+        static const uint32_t K[64] = {
+            0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+            0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+            0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+            0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+            0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+            0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+            0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+            0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+        uint32_t w[64];
+        for (int i = 0; i < 16; ++i)
+            w[i] = (uint32_t(p[4 * i]) << 24) | (uint32_t(p[4 * i + 1]) << 16) | (uint32_t(p[4 * i + 2]) << 8) |
+                   uint32_t(p[4 * i + 3]);
+        for (int i = 16; i < 64; ++i) {
+            const uint32_t s0 = ror(w[i - 15], 7) ^ ror(w[i - 15], 18) ^ (w[i - 15] >> 3);
+            const uint32_t s1 = ror(w[i - 2], 17) ^ ror(w[i - 2], 19) ^ (w[i - 2] >> 10);
+            w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+        }
+        uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+        for (int i = 0; i < 64; ++i) {
+            const uint32_t S1 = ror(e, 6) ^ ror(e, 11) ^ ror(e, 25);
+            const uint32_t ch = (e & f) ^ (~e & g);
+            const uint32_t t1 = hh + S1 + ch + K[i] + w[i];
+            const uint32_t S0 = ror(a, 2) ^ ror(a, 13) ^ ror(a, 22);
+            const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+            const uint32_t t2 = S0 + mj;
+            hh = g;
+            g = f;
+            f = e;
+            e = d + t1;
+            d = c;
+            c = b;
+            b = a;
+            a = t1 + t2;
+        }
+        h[0] += a;
+        h[1] += b;
+        h[2] += c;
+        h[3] += d;
+        h[4] += e;
+        h[5] += f;
+        h[6] += g;
+        h[7] += hh;
+    }
+    void update(const uint8_t* p, size_t n) {
+        total += n;
+        while (n > 0) {
+            const size_t take = std::min(n, 64 - fill);
+            std::memcpy(buf + fill, p, take);
+            fill += take;
+            p += take;
+            n -= take;
+            if (fill == 64) {
+                block(buf);
+                fill = 0;
+            }
+        }
+    }
+    void final(uint8_t out[32]) {
+        const uint64_t bits = total * 8;
+        const uint8_t one = 0x80, zero = 0;
+        update(&one, 1);
+        while (fill != 56) update(&zero, 1);
+        uint8_t len[8];
+        for (int i = 0; i < 8; ++i) len[i] = uint8_t(bits >> (56 - 8 * i));
+        update(len, 8);
+        for (int i = 0; i < 8; ++i) {
+            out[4 * i] = uint8_t(h[i] >> 24);
+            out[4 * i + 1] = uint8_t(h[i] >> 16);
+            out[4 * i + 2] = uint8_t(h[i] >> 8);
+            out[4 * i + 3] = uint8_t(h[i]);
+        }
+    }
+};
+
+// ---------------------------------------------------------------- canonical bytes (detcore.cpp:73-84)
+static void put_le32(std::vector<uint8_t>& o, uint32_t v) {
+    o.push_back(uint8_t(v));
+    o.push_back(uint8_t(v >> 8));
+    o.push_back(uint8_t(v >> 16));
+    o.push_back(uint8_t(v >> 24));
+}
+static void put_be32(std::vector<uint8_t>& o, uint32_t v) {
+    o.push_back(uint8_t(v >> 24));
+    o.push_back(uint8_t(v >> 16));
+    o.push_back(uint8_t(v >> 8));
+    o.push_back(uint8_t(v));
+}
+static std::vector<uint8_t> encode_canonical(const uint32_t* tokens, uint32_t T, const float* logits, uint32_t V) {
+    std::vector<uint8_t> out;
+    out.reserve(8 + 4 * size_t(T) + size_t(T) * (4 + 4 * size_t(V)));
+    put_le32(out, T);
+    for (uint32_t i = 0; i < T; ++i) put_le32(out, tokens[i]);
+    put_le32(out, T);
+    for (uint32_t s = 0; s < T; ++s) {
+        put_le32(out, V);
+        for (uint32_t i = 0; i < V; ++i) {
+            uint32_t b;
+            std::memcpy(&b, logits + size_t(s) * V + i, 4);
+            put_le32(out, b);
+        }
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------- ToyModel (detcore.cpp:264-315)
+constexpr uint32_t kToyVocab = 32, kToyDim = 16;
+struct Toy {
+    std::vector<float> embed, recur, hidden, project;
+};
+static std::vector<float> gen_weights(Prng& prng, size_t count) {
+    std::vector<float> w(count);
+    for (auto& v : w) {
+        float u = prng.next_symmetric_f32();
+        int e = int(prng.next_below(7)) - 3;
+        v = std::ldexp(u, e);
+    }
+    return w;
+}
+static Toy toy_from_model_id(const char* model_id) {
+    Toy m;
+    Prng prng = Prng::seeded(fnv1a64(model_id));
+    m.embed = gen_weights(prng, size_t(kToyVocab) * kToyDim);
+    m.recur = gen_weights(prng, size_t(kToyDim) * kToyDim);
+    m.hidden = gen_weights(prng, size_t(kToyDim) * kToyDim);
+    m.project = gen_weights(prng, size_t(kToyVocab) * kToyDim);
+    return m;
+}
+// det_matvec (detcore.cpp:165-185); arch 0 = archA (tree), 1 = archB (sequential, split)
+static std::vector<float> det_matvec(const std::vector<float>& M, size_t rows, size_t cols, const std::vector<float>& v,
+                                     int arch) {
+    std::vector<float> out(rows), prod(cols);
+    for (size_t r = 0; r < rows; ++r) {
+        const float* row = M.data() + r * cols;
+        for (size_t c = 0; c < cols; ++c) prod[c] = row[c] * v[c];
+        out[r] = arch == 0 ? tree_reduce(prod.data(), cols) : sequential_reduce(prod.data(), cols);
+    }
+    return out;
+}
+static float softsign(float x) { return x / (1.0f + std::fabs(x)); }
+
+static int toy_infer(const char* model_id, int arch, const uint32_t* prompt, uint32_t plen, const Policy& pol,
+                     uint64_t seed, uint32_t* tokens_out, float* logits_out) {
+    if (arch != 0 && arch != 1) return 1;
+    if (!pol.valid()) return 1;
+    for (uint32_t i = 0; i < plen; ++i)
+        if (prompt[i] >= kToyVocab) return 1;
+    const Toy m = toy_from_model_id(model_id);
+    std::vector<float> state(kToyDim, 0.0f);
+    auto advance = [&](uint32_t tok) {
+        std::vector<float> next = det_matvec(m.recur, kToyDim, kToyDim, state, arch);
+        const float* emb = m.embed.data() + size_t(tok) * kToyDim;
+        for (size_t i = 0; i < kToyDim; ++i) next[i] = softsign(next[i] + emb[i]);
+        state = next;
+    };
+    for (uint32_t i = 0; i < plen; ++i) advance(prompt[i]);
+    Prng prng = Prng::seeded(seed);
+    std::vector<float> probs(kToyVocab);
+    for (uint32_t t = 0; t < pol.max_tokens; ++t) {
+        std::vector<float> h = det_matvec(m.hidden, kToyDim, kToyDim, state, arch);
+        for (auto& v : h) v = softsign(v);
+        std::vector<float> logits = det_matvec(m.project, kToyVocab, kToyDim, h, arch);
+        if (!det_softmax(logits.data(), kToyVocab, probs.data())) return 4;
+        const float r = prng.next_unit_f32();
+        const int64_t tok = decode_with_draw(probs.data(), kToyVocab, pol, r);
+        if (tok < 0) return 1;
+        tokens_out[t] = uint32_t(tok);
+        std::memcpy(logits_out + size_t(t) * kToyVocab, logits.data(), sizeof(float) * kToyVocab);
+        advance(uint32_t(tok));
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------- Llama-style transformer
+static inline uint16_t bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return uint16_t(u >> 16);
+}
+static inline float bf2f(uint16_t b) {
+    uint32_t u = uint32_t(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+struct Config {
+    const char* name;
+    int L, d, hq, hkv, hd, F, V;
+    double theta;
+    float eps;
+};
+static const Config kConfigs[] = {
+    {"llama-tiny", 2, 256, 4, 2, 64, 768, 4096, 500000.0, 1e-5f},
+    {"llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 500000.0, 1e-5f},
+};
+static const Config* find_config(const char* model_id) {
+    for (const auto& c : kConfigs) {
+        const size_t n = std::strlen(c.name);
+        if (std::strncmp(model_id, c.name, n) == 0 && (model_id[n] == 0 || model_id[n] == ':')) return &c;
+    }
+    return nullptr;
+}
+static int half_log2_round(int n) { return int(std::lround(0.5 * std::log2(double(n)))); }
+
+static int g_threads = 0;
+static int nthreads() {
+    if (g_threads > 0) return g_threads;
+    unsigned n = std::thread::hardware_concurrency();
+    return n == 0 ? 1 : int(n);
+}
+template <class F>
+static void parallel_for(int64_t n, F f) {
+    const int nt = int(std::min<int64_t>(nthreads(), std::max<int64_t>(1, n / 64)));
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::atomic<int64_t> next{0};
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            for (;;) {
+                const int64_t b = next.fetch_add(64);
+                if (b >= n) break;
+                const int64_t e = std::min<int64_t>(n, b + 64);
+                for (int64_t i = b; i < e; ++i) f(i);
+            }
+        });
+    for (auto& t : th) t.join();
+}
+
+// Counter-based tensor generation: element i of tensor t:
+//   z = splitmix64 output i+1 from seed_t ; u = float(z>>40)*2^-23 - 1 ; w = bf16(u*2^e) | bf16(fma(u,1/8,1))
+static void gen_tensor(uint64_t seed, int64_t rows, int64_t cols, int scale_exp, bool gamma, uint16_t* out) {
+    const float scale = std::ldexp(1.0f, scale_exp);
+    parallel_for(rows, [&](int64_t r) {
+        for (int64_t c = 0; c < cols; ++c) {
+            const uint64_t i = uint64_t(r * cols + c);
+            uint64_t x = seed + i * 0x9E3779B97F4A7C15ULL;   // splitmix64 state after i steps
+            const uint64_t z = splitmix64(x);
+            const float u = float(z >> 40) * 0x1.0p-23f - 1.0f;
+            const float v = gamma ? std::fmaf(u, 0.125f, 1.0f) : u * scale;
+            out[r * cols + c] = bf16_rne(v);
+        }
+    });
+}
+
+struct Llama {
+    Config cfg;
+    uint64_t base_seed;
+    std::vector<uint16_t> embed, lm_head, final_norm;
+    struct Layer {
+        std::vector<uint16_t> attn_norm, wq, wk, wv, wo, ffn_norm, wg, wu, wd;
+    };
+    std::vector<Layer> layers;
+    std::vector<float> rope_cos, rope_sin;   // [pos][hd/2]
+    int max_pos = 0;
+
+    uint64_t tseed(int tid) const { return mix_seed(base_seed, uint64_t(tid)); }
+    void ensure_rope(int npos) {
+        if (npos <= max_pos) return;
+        const int h2 = cfg.hd / 2;
+        rope_cos.resize(size_t(npos) * h2);
+        rope_sin.resize(size_t(npos) * h2);
+        for (int p = max_pos; p < npos; ++p)
+            for (int i = 0; i < h2; ++i) {
+                const double inv = std::pow(cfg.theta, -2.0 * i / cfg.hd);
+                const double ang = double(p) * inv;
+                rope_cos[size_t(p) * h2 + i] = float(std::cos(ang));
+                rope_sin[size_t(p) * h2 + i] = float(std::sin(ang));
+            }
+        max_pos = npos;
+    }
+};
+
+static Llama* llama_new(const char* model_id) {
+    const Config* c = find_config(model_id);
+    if (c == nullptr) return nullptr;
+    Llama* m = new Llama();
+    m->cfg = *c;
+    m->base_seed = fnv1a64(model_id);
+    const int d = c->d, qd = c->hq * c->hd, kd = c->hkv * c->hd, F = c->F, V = c->V;
+    const int sd = -half_log2_round(d), sq = -half_log2_round(qd), sf = -half_log2_round(F);
+    m->embed.resize(size_t(V) * d);
+    gen_tensor(m->tseed(0), V, d, 0, false, m->embed.data());
+    m->lm_head.resize(size_t(V) * d);
+    gen_tensor(m->tseed(1), V, d, 4 + sd, false, m->lm_head.data());
+    m->final_norm.resize(d);
+    gen_tensor(m->tseed(2), 1, d, 0, true, m->final_norm.data());
+    m->layers.resize(c->L);
+    for (int l = 0; l < c->L; ++l) {
+        auto& Ly = m->layers[l];
+        const int b = 16 + 16 * l;
+        Ly.attn_norm.resize(d);
+        gen_tensor(m->tseed(b + 0), 1, d, 0, true, Ly.attn_norm.data());
+        Ly.wq.resize(size_t(qd) * d);
+        gen_tensor(m->tseed(b + 1), qd, d, sd, false, Ly.wq.data());
+        Ly.wk.resize(size_t(kd) * d);
+        gen_tensor(m->tseed(b + 2), kd, d, sd, false, Ly.wk.data());
+        Ly.wv.resize(size_t(kd) * d);
+        gen_tensor(m->tseed(b + 3), kd, d, sd, false, Ly.wv.data());
+        Ly.wo.resize(size_t(d) * qd);
+        gen_tensor(m->tseed(b + 4), d, qd, sq, false, Ly.wo.data());
+        Ly.ffn_norm.resize(d);
+        gen_tensor(m->tseed(b + 5), 1, d, 0, true, Ly.ffn_norm.data());
+        Ly.wg.resize(size_t(F) * d);
+        gen_tensor(m->tseed(b + 6), F, d, sd, false, Ly.wg.data());
+        Ly.wu.resize(size_t(F) * d);
+        gen_tensor(m->tseed(b + 7), F, d, sd, false, Ly.wu.data());
+        Ly.wd.resize(size_t(d) * F);
+        gen_tensor(m->tseed(b + 8), d, F, sf, false, Ly.wd.data());
+    }
+    return m;
+}
+
+// y[r] = tree_c(W[r,c] * x[c]) — det_matvec canonical_tree (detcore.cpp:180-181); products of two
+// bf16 values are exact in f32.
+static void gemv(const uint16_t* W, int rows, int cols, const uint16_t* x, float* y) {
+    parallel_for(rows, [&](int64_t r) {
+        thread_local std::vector<float> prod;
+        prod.resize(cols);
+        const uint16_t* w = W + size_t(r) * cols;
+        for (int c = 0; c < cols; ++c) prod[c] = bf2f(w[c]) * bf2f(x[c]);
+        y[r] = tree_reduce(prod.data(), cols);
+    });
+}
+
+static void rmsnorm(const float* x, const uint16_t* gamma, int d, float eps, uint16_t* out) {
+    std::vector<float> sq(d);
+    for (int i = 0; i < d; ++i) sq[i] = x[i] * x[i];
+    const float ss = tree_reduce(sq.data(), d);
+    const float ms = ss / float(d);
+    const float rstd = 1.0f / std::sqrt(ms + eps);
+    for (int i = 0; i < d; ++i) out[i] = bf16_rne((x[i] * rstd) * bf2f(gamma[i]));
+}
+
+constexpr int kChunk = 128;
+// Attention for one query head against positions [0, ctx) of a contiguous cache k[p][hd], v[p][hd]
+// (DESIGN.md §3.5): fixed 128-position chunks, tree-summed dot products and chunk sums, fma chains
+// for the weighted values, chunk-order combine.
+static void attention_head(const uint16_t* q, const uint16_t* const* kp, const uint16_t* const* vp, int ctx, int hd,
+                           float scale, uint16_t* out) {
+    const int nch = (ctx + kChunk - 1) / kChunk;
+    std::vector<float> m(nch), l(nch), o(size_t(nch) * hd);
+    std::vector<float> prod(hd), s(kChunk), e(kChunk);
+    for (int c = 0; c < nch; ++c) {
+        const int p0 = c * kChunk, n = std::min(kChunk, ctx - p0);
+        for (int j = 0; j < n; ++j) {
+            for (int dd = 0; dd < hd; ++dd) prod[dd] = bf2f(q[dd]) * bf2f(kp[p0 + j][dd]);
+            s[j] = tree_reduce(prod.data(), hd) * scale;
+        }
+        float mx = s[0];
+        for (int j = 0; j < n; ++j) mx = std::max(mx, s[j]);
+        for (int j = 0; j < n; ++j) e[j] = det_expf(s[j] - mx);
+        m[c] = mx;
+        l[c] = tree_reduce(e.data(), n);
+        for (int dd = 0; dd < hd; ++dd) {
+            float acc = 0.0f;
+            for (int j = 0; j < n; ++j) acc = std::fmaf(e[j], bf2f(vp[p0 + j][dd]), acc);
+            o[size_t(c) * hd + dd] = acc;
+        }
+    }
+    float M = m[0];
+    for (int c = 0; c < nch; ++c) M = std::max(M, m[c]);
+    std::vector<float> al(nch);
+    float L = 0.0f;
+    for (int c = 0; c < nch; ++c) {
+        al[c] = det_expf(m[c] - M);
+        L = std::fmaf(l[c], al[c], L);
+    }
+    for (int dd = 0; dd < hd; ++dd) {
+        float O = 0.0f;
+        for (int c = 0; c < nch; ++c) O = std::fmaf(o[size_t(c) * hd + dd], al[c], O);
+        out[dd] = bf16_rne(O / L);
+    }
+}
+
+struct Session {
+    const Llama* m;
+    std::vector<std::vector<uint16_t>> kc, vc;   // per layer: [pos][hkv*hd]
+    int pos = 0;
+};
+
+// One token through the stack at position s.pos; returns logits if want_logits.
+static void forward_token(Session& s, uint32_t token, bool want_logits, float* logits) {
+    const Llama& m = *s.m;
+    const Config& c = m.cfg;
+    const int d = c.d, hd = c.hd, qd = c.hq * hd, kd = c.hkv * hd, F = c.F, G = c.hq / c.hkv;
+    const int pos = s.pos;
+    const float scale = float(1.0 / std::sqrt(double(hd)));
+    std::vector<float> x(d);
+    for (int i = 0; i < d; ++i) x[i] = bf2f(m.embed[size_t(token) * d + i]);
+    std::vector<uint16_t> h(d), qb(qd), attn(qd), act(F);
+    std::vector<float> q(qd), k(kd), v(kd), o(d), g(F), u(F), dn(d);
+    const float* cs = m.rope_cos.data() + size_t(pos) * (hd / 2);
+    const float* sn = m.rope_sin.data() + size_t(pos) * (hd / 2);
+    for (int l = 0; l < c.L; ++l) {
+        const auto& Ly = m.layers[l];
+        rmsnorm(x.data(), Ly.attn_norm.data(), d, c.eps, h.data());
+        gemv(Ly.wq.data(), qd, d, h.data(), q.data());
+        gemv(Ly.wk.data(), kd, d, h.data(), k.data());
+        gemv(Ly.wv.data(), kd, d, h.data(), v.data());
+        for (int vec = 0; vec < 2; ++vec) {
+            float* arr = vec == 0 ? q.data() : k.data();
+            const int nh = vec == 0 ? c.hq : c.hkv;
+            for (int hh = 0; hh < nh; ++hh)
+                for (int i = 0; i < hd / 2; ++i) {
+                    float* p = arr + hh * hd + 2 * i;
+                    const float x0 = p[0], x1 = p[1];
+                    p[0] = x0 * cs[i] - x1 * sn[i];
+                    p[1] = x0 * sn[i] + x1 * cs[i];
+                }
+        }
+        for (int i = 0; i < qd; ++i) qb[i] = bf16_rne(q[i]);
+        std::vector<uint16_t> kb(kd), vb(kd);
+        for (int i = 0; i < kd; ++i) {
+            kb[i] = bf16_rne(k[i]);
+            vb[i] = bf16_rne(v[i]);
+        }
+        s.kc[l].insert(s.kc[l].end(), kb.begin(), kb.end());
+        s.vc[l].insert(s.vc[l].end(), vb.begin(), vb.end());
+        const int ctx = pos + 1;
+        parallel_for(c.hq, [&](int64_t hh) {
+            const int kvh = int(hh) / G;
+            std::vector<const uint16_t*> kp(ctx), vp(ctx);
+            for (int p = 0; p < ctx; ++p) {
+                kp[p] = s.kc[l].data() + size_t(p) * kd + size_t(kvh) * hd;
+                vp[p] = s.vc[l].data() + size_t(p) * kd + size_t(kvh) * hd;
+            }
+            attention_head(qb.data() + hh * hd, kp.data(), vp.data(), ctx, hd, scale, attn.data() + hh * hd);
+        });
+        gemv(Ly.wo.data(), d, qd, attn.data(), o.data());
+        for (int i = 0; i < d; ++i) x[i] = x[i] + o[i];
+        rmsnorm(x.data(), Ly.ffn_norm.data(), d, c.eps, h.data());
+        gemv(Ly.wg.data(), F, d, h.data(), g.data());
+        gemv(Ly.wu.data(), F, d, h.data(), u.data());
+        for (int i = 0; i < F; ++i) {
+            const float e = det_expf(-g[i]);
+            const float sg = g[i] / (1.0f + e);
+            act[i] = bf16_rne(sg * u[i]);
+        }
+        gemv(Ly.wd.data(), d, F, act.data(), dn.data());
+        for (int i = 0; i < d; ++i) x[i] = x[i] + dn[i];
+    }
+    s.pos++;
+    if (!want_logits) return;
+    rmsnorm(x.data(), m.final_norm.data(), d, c.eps, h.data());
+    gemv(m.lm_head.data(), c.V, d, h.data(), logits);
+}
+
+}  // namespace orc
+
+using namespace orc;
+
+// ==================================================================== C API (ctypes)
+extern "C" {
+
+void orc_set_threads(int n) { g_threads = n; }
+int orc_get_threads(void) { return nthreads(); }
+uint64_t orc_fnv1a64(const char* s) { return fnv1a64(s); }
+uint64_t orc_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
+void orc_prng_seeded(uint64_t seed, uint64_t* st) {
+    Prng p = Prng::seeded(seed);
+    std::memcpy(st, p.s, 32);
+}
+uint64_t orc_prng_next_u64(uint64_t* st) {
+    Prng p;
+    std::memcpy(p.s, st, 32);
+    const uint64_t r = p.next_u64();
+    std::memcpy(st, p.s, 32);
+    return r;
+}
+uint64_t orc_prng_next_below(uint64_t* st, uint64_t bound) {
+    Prng p;
+    std::memcpy(p.s, st, 32);
+    const uint64_t r = p.next_below(bound);
+    std::memcpy(st, p.s, 32);
+    return r;
+}
+float orc_prng_next_unit_f32(uint64_t* st) {
+    Prng p;
+    std::memcpy(p.s, st, 32);
+    const float r = p.next_unit_f32();
+    std::memcpy(st, p.s, 32);
+    return r;
+}
+float orc_tree_reduce(const float* v, size_t n) { return tree_reduce(v, n); }
+float orc_seq_reduce(const float* v, size_t n) { return sequential_reduce(v, n); }
+float orc_expf(float x) { return det_expf(x); }
+void orc_expf_array(const float* x, float* y, size_t n) {
+    for (size_t i = 0; i < n; ++i) y[i] = det_expf(x[i]);
+}
+void orc_libm_expf_array(const float* x, float* y, size_t n) {
+    for (size_t i = 0; i < n; ++i) y[i] = std::exp(x[i]);
+}
+int orc_softmax(const float* logits, size_t n, float* out) { return det_softmax(logits, n, out) ? 0 : 1; }
+int64_t orc_decode_with_draw(const float* probs, size_t n, int kind, int has_k, uint32_t k, int has_p, float p,
+                             float r) {
+    Policy pol;
+    pol.kind = kind;
+    pol.has_k = has_k;
+    pol.k = k;
+    pol.has_p = has_p;
+    pol.p = p;
+    return decode_with_draw(probs, n, pol, r);
+}
+void orc_sha256(const uint8_t* data, size_t n, uint8_t* out) {
+    Sha256 h;
+    h.update(data, n);
+    h.final(out);
+}
+size_t orc_canonical_size(uint32_t T, uint32_t V) { return 8 + 4 * size_t(T) + size_t(T) * (4 + 4 * size_t(V)); }
+void orc_encode_canonical(const uint32_t* tokens, uint32_t T, const float* logits, uint32_t V, uint8_t* out) {
+    auto b = encode_canonical(tokens, T, logits, V);
+    std::memcpy(out, b.data(), b.size());
+}
+// codec.cpp:67-104 (Writer: str = be32 len + bytes, hash = 32 raw bytes, policy, be64 seed, prompt)
+size_t orc_encode_exec_tuple(const char* model_id, const uint8_t* digest, const char* arch, const char* driver,
+                             int kind, int has_k, uint32_t k, int has_p, float p, uint32_t max_tokens, uint64_t seed,
+                             const uint32_t* prompt, uint32_t plen, uint8_t* out) {
+    std::vector<uint8_t> w;
+    auto str = [&](const char* s) {
+        const size_t n = std::strlen(s);
+        put_be32(w, uint32_t(n));
+        w.insert(w.end(), s, s + n);
+    };
+    str(model_id);
+    w.insert(w.end(), digest, digest + 32);
+    str(arch);
+    str(driver);
+    w.push_back(uint8_t(kind));
+    w.push_back(has_k ? 1 : 0);
+    put_be32(w, has_k ? k : 0);
+    w.push_back(has_p ? 1 : 0);
+    uint32_t pb = 0;
+    const float pv = has_p ? p : 0.0f;
+    std::memcpy(&pb, &pv, 4);
+    put_be32(w, pb);
+    put_be32(w, max_tokens);
+    put_be32(w, uint32_t(seed >> 32));
+    put_be32(w, uint32_t(seed));
+    put_be32(w, plen);
+    for (uint32_t i = 0; i < plen; ++i) put_be32(w, prompt[i]);
+    if (out != nullptr) std::memcpy(out, w.data(), w.size());
+    return w.size();
+}
+
+int orc_toy_infer(const char* model_id, int arch, const uint32_t* prompt, uint32_t plen, int kind, int has_k,
+                  uint32_t k, int has_p, float p, uint32_t max_tokens, uint64_t seed, uint32_t* tokens_out,
+                  float* logits_out) {
+    Policy pol;
+    pol.kind = kind;
+    pol.has_k = has_k;
+    pol.k = k;
+    pol.has_p = has_p;
+    pol.p = p;
+    pol.max_tokens = max_tokens;
+    return toy_infer(model_id, arch, prompt, plen, pol, seed, tokens_out, logits_out);
+}
+
+void orc_gen_tensor(uint64_t seed, int64_t rows, int64_t cols, int scale_exp, int is_gamma, uint16_t* out) {
+    gen_tensor(seed, rows, cols, scale_exp, is_gamma != 0, out);
+}
+void orc_rmsnorm(const float* x, const uint16_t* gamma, int d, float eps, uint16_t* out) {
+    rmsnorm(x, gamma, d, eps, out);
+}
+// q [hd] bf16, k/v contiguous [ctx][hd] bf16 for one kv head
+void orc_attention_head(const uint16_t* q, const uint16_t* k, const uint16_t* v, int ctx, int hd, uint16_t* out) {
+    std::vector<const uint16_t*> kp(ctx), vp(ctx);
+    for (int p = 0; p < ctx; ++p) {
+        kp[p] = k + size_t(p) * hd;
+        vp[p] = v + size_t(p) * hd;
+    }
+    attention_head(q, kp.data(), vp.data(), ctx, hd, float(1.0 / std::sqrt(double(hd))), out);
+}
+void orc_rope_table(double theta, int hd, int npos, float* cos_out, float* sin_out) {
+    for (int p = 0; p < npos; ++p)
+        for (int i = 0; i < hd / 2; ++i) {
+            const double inv = std::pow(theta, -2.0 * i / hd);
+            const double ang = double(p) * inv;
+            cos_out[size_t(p) * (hd / 2) + i] = float(std::cos(ang));
+            sin_out[size_t(p) * (hd / 2) + i] = float(std::sin(ang));
+        }
+}
+
+void* orc_llama_new(const char* model_id) { return llama_new(model_id); }
+void orc_llama_free(void* h) { delete static_cast<Llama*>(h); }
+// fields: L, d, hq, hkv, hd, F, V
+void orc_llama_info(void* h, int* f) {
+    const Config& c = static_cast<Llama*>(h)->cfg;
+    f[0] = c.L;
+    f[1] = c.d;
+    f[2] = c.hq;
+    f[3] = c.hkv;
+    f[4] = c.hd;
+    f[5] = c.F;
+    f[6] = c.V;
+}
+uint64_t orc_llama_tensor_seed(void* h, int tid) { return static_cast<Llama*>(h)->tseed(tid); }
+const uint16_t* orc_llama_tensor(void* h, int which, int layer) {
+    Llama* m = static_cast<Llama*>(h);
+    switch (which) {
+        case 0: return m->embed.data();
+        case 1: return m->lm_head.data();
+        case 2: return m->final_norm.data();
+        default: break;
+    }
+    const auto& L = m->layers[layer];
+    switch (which) {
+        case 3: return L.attn_norm.data();
+        case 4: return L.wq.data();
+        case 5: return L.wk.data();
+        case 6: return L.wv.data();
+        case 7: return L.wo.data();
+        case 8: return L.ffn_norm.data();
+        case 9: return L.wg.data();
+        case 10: return L.wu.data();
+        case 11: return L.wd.data();
+        default: return nullptr;
+    }
+}
+
+// Teacher-forced: feed tokens[0..n) and write logits after each position >= first_logit_pos
+// into logits_out[(i - first_logit_pos) * V].
+int orc_llama_teacher(void* h, const uint32_t* tokens, int n, int first_logit_pos, float* logits_out) {
+    Llama* m = static_cast<Llama*>(h);
+    m->ensure_rope(n + 1);
+    Session s{m, std::vector<std::vector<uint16_t>>(m->cfg.L), std::vector<std::vector<uint16_t>>(m->cfg.L), 0};
+    for (int i = 0; i < n; ++i) {
+        if (tokens[i] >= uint32_t(m->cfg.V)) return 1;
+        const bool want = i >= first_logit_pos;
+        forward_token(s, tokens[i], want, want ? logits_out + size_t(i - first_logit_pos) * m->cfg.V : nullptr);
+    }
+    return 0;
+}
+
+// Full reference-semantics inference: prefill prompt, then max_tokens decode steps with the
+// reference's softmax / decode rules; logits_out [max_tokens][V] (required).
+int orc_llama_generate(void* h, const uint32_t* prompt, uint32_t plen, int kind, int has_k, uint32_t k, int has_p,
+                       float p, uint32_t max_tokens, uint64_t seed, uint32_t* tokens_out, float* logits_out) {
+    Llama* m = static_cast<Llama*>(h);
+    Policy pol;
+    pol.kind = kind;
+    pol.has_k = has_k;
+    pol.k = k;
+    pol.has_p = has_p;
+    pol.p = p;
+    pol.max_tokens = max_tokens;
+    if (!pol.valid()) return 1;
+    if (plen == 0) return 1;
+    for (uint32_t i = 0; i < plen; ++i)
+        if (prompt[i] >= uint32_t(m->cfg.V)) return 1;
+    if (max_tokens == 0) return 0;
+    const int V = m->cfg.V;
+    m->ensure_rope(int(plen + max_tokens));
+    Session s{m, std::vector<std::vector<uint16_t>>(m->cfg.L), std::vector<std::vector<uint16_t>>(m->cfg.L), 0};
+    for (uint32_t i = 0; i + 1 < plen; ++i) forward_token(s, prompt[i], false, nullptr);
+    forward_token(s, prompt[plen - 1], true, logits_out);
+    Prng prng = Prng::seeded(seed);
+    std::vector<float> probs(V);
+    for (uint32_t t = 0; t < max_tokens; ++t) {
+        float* lg = logits_out + size_t(t) * V;
+        if (!det_softmax(lg, V, probs.data())) return 4;
+        const float r = prng.next_unit_f32();
+        const int64_t tok = decode_with_draw(probs.data(), V, pol, r);
+        if (tok < 0) return 1;
+        tokens_out[t] = uint32_t(tok);
+        if (t + 1 < max_tokens) forward_token(s, uint32_t(tok), true, logits_out + size_t(t + 1) * V);
+    }
+    return 0;
+}
+
+}  // extern "C"

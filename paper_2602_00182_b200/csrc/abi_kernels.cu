@@ -1,0 +1,137 @@
+// Kernel-level C-ABI entry points (device pointers). The parity tests call the same kernels the
+// engine launches, through these wrappers, and compare with the CPU oracle.
+#include <mutex>
+#include <vector>
+#include <string>
+#include <unordered_map>
+
+#include "common.h"
+#include "detgpu.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace detgpu {
+
+static std::mutex g_err_mu;
+static std::string g_err;
+void set_global_error(const std::string& msg) {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    g_err = msg;
+}
+const std::string& global_error() {
+    return g_err;
+}
+
+}  // namespace detgpu
+
+using namespace detgpu;
+
+extern "C" {
+
+const char* detgpu_version(void) { return "detgpu 0.1 (sm_100a, tcgen05)"; }
+
+const char* detgpu_global_error(void) { return detgpu::global_error().c_str(); }
+
+int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy, void* stream) {
+    CUtensorMap tw, tx;
+    if (!make_tmap_bf16(&tw, W, K, n_out, 128) || !make_tmap_bf16(&tx, X, K, ncols, 64)) {
+        set_global_error("cuTensorMapEncodeTiled failed");
+        return DETGPU_ECUDA;
+    }
+    GemmParams p{};
+    p.n_out = n_out;
+    p.k = K;
+    p.ncols = ncols;
+    p.mode = kEpiStoreF32;
+    p.out = Y;
+    p.ld_out = ldy;
+    DETGPU_CUDA_TRY(gemm_launch(tw, tx, p, static_cast<cudaStream_t>(stream), false));
+    return DETGPU_OK;
+}
+
+int detgpu_k_rmsnorm(const float* x, const void* gamma, void* out, int ncols, int d, float eps, void* stream) {
+    DETGPU_CUDA_TRY(launch_rmsnorm(x, nullptr, nullptr, nullptr, static_cast<const __nv_bfloat16*>(gamma),
+                                   static_cast<__nv_bfloat16*>(out), nullptr, ncols, d, eps,
+                                   static_cast<cudaStream_t>(stream), false));
+    return DETGPU_OK;
+}
+
+int detgpu_k_expf(const float* x, float* y, int64_t n, void* stream) {
+    DETGPU_CUDA_TRY(launch_expf(x, y, n, static_cast<cudaStream_t>(stream)));
+    return DETGPU_OK;
+}
+
+int detgpu_k_tree_sum(const float* x, float* out, int rows, int n, void* stream) {
+    DETGPU_CUDA_TRY(launch_tree_sum(x, out, rows, n, static_cast<cudaStream_t>(stream)));
+    return DETGPU_OK;
+}
+
+int detgpu_k_init_tensor(void* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp, int is_gamma,
+                         int row_mul, int row_add, void* stream) {
+    DETGPU_CUDA_TRY(launch_init_tensor(static_cast<__nv_bfloat16*>(dst), seed, rows, cols, scale_exp, is_gamma,
+                                       row_mul, row_add, static_cast<cudaStream_t>(stream)));
+    return DETGPU_OK;
+}
+
+int detgpu_k_attention(const void* q, const void* kcache, const void* vcache, const int32_t* block_table,
+                       const int32_t* col_pos, const int32_t* col_req, void* out, int ncols, int hq, int hkv,
+                       int hd, int page, int max_pages, void* stream) {
+    AttnParams a{};
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.kcache = static_cast<const __nv_bfloat16*>(kcache);
+    a.vcache = static_cast<const __nv_bfloat16*>(vcache);
+    a.block_table = block_table;
+    a.col_pos = col_pos;
+    a.col_req = col_req;
+    a.out = static_cast<__nv_bfloat16*>(out);
+    a.ncols = ncols;
+    a.hq = hq;
+    a.hkv = hkv;
+    a.hd = hd;
+    a.page = page;
+    a.max_pages = max_pages;
+    // chunk grid sized from the cache capacity so that the launch shape never depends on data
+    a.max_chunks = (max_pages * page + kAttnChunk - 1) / kAttnChunk;
+    float* ws = nullptr;
+    const size_t ws_bytes = attn_workspace_bytes(a);
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, static_cast<cudaStream_t>(stream)));
+    a.ws = ws;
+    cudaError_t e = launch_attention(a, static_cast<cudaStream_t>(stream), false);
+    cudaFreeAsync(ws, static_cast<cudaStream_t>(stream));
+    DETGPU_CUDA_TRY(e);
+    return DETGPU_OK;
+}
+
+int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_policy* policies, uint64_t* prng_state,
+                    uint32_t* tokens_out, float* probs_out, int32_t* status_out, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    SampleParams sp{};
+    DevPolicy* dpol = nullptr;
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dpol), sizeof(DevPolicy) * rows, s));
+    std::vector<DevPolicy> hp(rows);
+    for (int i = 0; i < rows; ++i) hp[i] = to_dev_policy(policies[i]);
+    DETGPU_CUDA_TRY(cudaMemcpyAsync(dpol, hp.data(), sizeof(DevPolicy) * rows, cudaMemcpyHostToDevice, s));
+    float* probs = probs_out;
+    if (probs == nullptr) DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&probs), sizeof(float) * rows * (size_t)vocab, s));
+    uint64_t* keys = nullptr;
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&keys), sample_scratch_bytes(rows, vocab), s));
+    sp.logits = logits;
+    sp.logit_row_stride = vocab;
+    sp.rows = rows;
+    sp.vocab = vocab;
+    sp.policy = dpol;
+    sp.prng = prng_state;
+    sp.probs = probs;
+    sp.scratch = keys;
+    sp.token_out = tokens_out;
+    sp.status = status_out;
+    cudaError_t e = launch_sample(sp, s, false);
+    cudaFreeAsync(keys, s);
+    if (probs_out == nullptr) cudaFreeAsync(probs, s);
+    cudaFreeAsync(dpol, s);
+    DETGPU_CUDA_TRY(e);
+    DETGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    return DETGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// Batch-invariant bf16 GEMM on tcgen05 (declarations shared by gemm.cu and the engine).
+//
+//   Y[col, n] = sum_k X[col, k] * W[n, k]      W: [n_out, K] bf16 (weights), X: [ncols, K] bf16
+//
+// Swap-AB: weight rows are the MMA M dimension (128 per CTA), activation columns (tokens) are the
+// MMA N dimension in fixed 64-wide sub-tiles. The instruction shape (M=128, N=64, K=16), the K
+// order (k-block 0..K/64-1, four K=16 steps each, accumulated in TMEM) and the tile of every column
+// are the same for every batch size: a column's bits depend only on its own activations and the
+// weights (tested by tests/test_gpu_gemm.py::test_batch_invariance).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace detgpu {
+
+enum GemmMode : int {
+    kEpiStoreF32 = 0,   // out[off(col) + row] = acc            (logits, generic)
+    kEpiAddF32 = 1,     // out[col*ld + row] += acc              (residual stream)
+    kEpiQkvRope = 2,    // RoPE(q,k) -> q bf16, k/v appended to the paged KV cache
+    kEpiSwiglu = 3,     // interleaved gate/up rows -> silu(g)*u bf16
+};
+
+struct GemmParams {
+    int n_out;   // rows of W (multiple of 128)
+    int k;       // reduction extent (multiple of 64)
+    int ncols;   // number of activation columns
+    int mode;
+    // kEpiStoreF32 / kEpiAddF32
+    float* out;
+    int64_t ld_out;            // per-column stride of `out` (elements)
+    const int* col_step;       // optional: logits trace step per column (<0 = inactive)
+    const int* col_slot;       // optional: request slot per column (with col_step)
+    int64_t slot_stride;       // elements per slot in the trace (with col_step)
+    // kEpiQkvRope
+    __nv_bfloat16* q_out;      // [ncols][hq*hd]
+    int hq, hkv, hd;
+    const int* col_pos;        // position of each column
+    const int* col_req;        // request slot of each column (block table row)
+    const float* rope_cos;     // [max_pos][hd/2]
+    const float* rope_sin;
+    __nv_bfloat16* kcache;     // this layer's K pool [pages][hkv][page][hd]
+    __nv_bfloat16* vcache;
+    const int* block_table;    // [slots][max_pages]
+    int max_pages;
+    int page;                  // positions per page
+    // kEpiSwiglu
+    __nv_bfloat16* act;        // [ncols][n_out/2]
+};
+
+// Tensor map for a row-major [rows, inner] bf16 matrix, box = 64 (inner) x box_rows, 128B swizzle.
+bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint32_t box_rows);
+
+// Launch (PDL-enabled) on `stream`. tmW: box 128 rows; tmX: box 64 rows.
+cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p,
+                        cudaStream_t stream, bool pdl);
+
+}  // namespace detgpu

@@ -1,0 +1,632 @@
+// Non-GEMM kernels: RMSNorm (+embedding gather), paged decode attention with a fixed KV-chunk
+// order, vocabulary softmax + decode (greedy / top-k / nucleus), counter-based weight generation.
+// Every reduction is a perfect binary tree over a -0.0f-padded power-of-two extent, which equals
+// the reference's canonical tree (detcore.cpp:135-150); every multiply-add is explicit.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "detmath.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace detgpu {
+
+namespace {
+
+__device__ __forceinline__ int next_pow2(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+// Perfect tree over [0, n) padded with -0 to P2 = max(128, pow2 >= n): 128-element tiles reduced by
+// one warp each (4 consecutive per lane, then the lane butterfly), tile sums reduced level by level
+// in shared memory. Requires blockDim.x == 1024 and n <= 131072.
+template <class Load>
+__device__ float block_tree_sum_1024(int n, Load ld, float* s_tiles) {
+    const int P2 = max(128, next_pow2(n));
+    const int ntiles = P2 / 128;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < ntiles; t += 32) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = t * 128 + lane * 4 + j;
+            v[j] = i < n ? ld(i) : kNegZero;
+        }
+        float s = local_tree_sum<4>(v);
+        s = warp_tree_sum(s);
+        if (lane == 0) s_tiles[t] = s;
+    }
+    __syncthreads();
+    for (int w = 1; w < ntiles; w <<= 1) {
+        for (int i = threadIdx.x * 2 * w; i < ntiles; i += blockDim.x * 2 * w)
+            s_tiles[i] = __fadd_rn(s_tiles[i], s_tiles[i + w]);
+        __syncthreads();
+    }
+    const float r = s_tiles[0];
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// y_i = bf16((x_i * rstd) * gamma_i), rstd = 1 / sqrt(tree(x*x)/d + eps)
+template <int E>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x_in, float* __restrict__ x_out,
+                                                      const __nv_bfloat16* __restrict__ embed,
+                                                      const int* __restrict__ col_token,
+                                                      const __nv_bfloat16* __restrict__ gamma,
+                                                      __nv_bfloat16* __restrict__ out, const int* __restrict__ col_index,
+                                                      int d, float eps) {
+    __shared__ float scratch[32];
+    pdl_trigger();
+    pdl_wait();
+    const int col = blockIdx.x;
+    const int base = threadIdx.x * E;
+    float v[E];
+    if (embed != nullptr) {
+        const int tok = col_token[col];
+        const __nv_bfloat16* src = embed + static_cast<int64_t>(tok) * d + base;
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = bf2f(src[j]);
+        float* dst = x_out + static_cast<int64_t>(col) * d + base;
+#pragma unroll
+        for (int j = 0; j < E; ++j) dst[j] = v[j];
+    } else {
+        const int row = col_index != nullptr ? col_index[col] : col;
+        const float* src = x_in + static_cast<int64_t>(row) * d + base;
+        if constexpr (E % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < E; j += 4) {
+                const float4 f = *reinterpret_cast<const float4*>(src + j);
+                v[j] = f.x;
+                v[j + 1] = f.y;
+                v[j + 2] = f.z;
+                v[j + 3] = f.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = src[j];
+        }
+    }
+    float sq[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) sq[j] = __fmul_rn(v[j], v[j]);
+    float s = local_tree_sum<E>(sq);
+    s = warp_tree_sum(s);
+    s = block_tree_combine<8>(s, scratch);
+    const float ms = __fdiv_rn(s, static_cast<float>(d));
+    const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
+    __nv_bfloat16* o = out + static_cast<int64_t>(col) * d + base;
+#pragma unroll
+    for (int j = 0; j < E; ++j) o[j] = f2bf(__fmul_rn(__fmul_rn(v[j], rstd), bf2f(gamma[base + j])));
+}
+
+// ------------------------------------------------------------------ misc test kernels
+__global__ void expf_kernel(const float* x, float* y, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        y[i] = det_expf(x[i]);
+}
+
+__global__ void __launch_bounds__(1024) tree_sum_kernel(const float* x, float* out, int n) {
+    __shared__ float tiles[1024];
+    const float* row = x + static_cast<int64_t>(blockIdx.x) * n;
+    const float s = block_tree_sum_1024(n, [&](int i) { return row[i]; }, tiles);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// ------------------------------------------------------------------ weights
+// Logical element (r, c) of a tensor seeded with `seed`: z = splitmix64 output r*cols+c+1;
+// u = (z >> 40) * 2^-23 - 1 in [-1, 1) (prng.hpp:68-70 next_symmetric_f32); value u * 2^scale_exp
+// (exact) or, for norm gains, fma(u, 1/8, 1); stored as bf16 (RNE) at physical row r*row_mul+row_add.
+__global__ void init_kernel(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, float scale,
+                            int is_gamma, int row_mul, int row_add) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t z = splitmix64_at(seed, static_cast<uint64_t>(i) + 1);
+        const float u = __fsub_rn(__fmul_rn(static_cast<float>(z >> 40), 0x1.0p-23f), 1.0f);
+        const float v = is_gamma ? __fmaf_rn(u, 0.125f, 1.0f) : __fmul_rn(u, scale);
+        const int64_t r = i / cols, c = i % cols;
+        dst[(r * row_mul + row_add) * cols + c] = f2bf(v);
+    }
+}
+
+// ------------------------------------------------------------------ attention
+// One CTA per (chunk, kv head, query column); G = hq/hkv query heads share the K/V chunk.
+//   s_p = tree_d(q_d * k_pd) * scale                 (products exact: bf16 x bf16)
+//   m = max_p s_p ; e_p = exp(s_p - m) ; l = tree_p(e_p) ; o_d = fma-chain_p(e_p * v_pd)
+// Partials (m, l, o) combined across chunks in chunk order by attn_combine_kernel.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_chunk_kernel(const AttnParams a, float scale) {
+    constexpr int CH = kAttnChunk;
+    constexpr int E = HD / 32;
+    extern __shared__ __align__(16) uint8_t attn_dsm[];
+    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_dsm);
+    __nv_bfloat16* sV = sK + CH * HD;
+    __shared__ float sQ[8 * HD];
+    __shared__ float sS[8 * CH];
+    __shared__ float sM[8], sL[8];
+    pdl_trigger();
+    const int c = blockIdx.x, kvh = blockIdx.y, col = blockIdx.z;
+    pdl_wait();
+    const int pos = a.col_pos[col];
+    if (pos < 0) return;
+    const int ctx = pos + 1;
+    const int p0 = c * CH;
+    if (p0 >= ctx) return;
+    const int n = min(CH, ctx - p0);
+    const int G = a.hq / a.hkv;
+    const int slot = a.col_req[col];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    for (int i = tid; i < G * HD; i += 128) sQ[i] = bf2f(qsrc[i]);
+    constexpr int VPR = HD * 2 / 16;   // 16-byte vectors per row
+    for (int i = tid; i < n * VPR; i += 128) {
+        const int r = i / VPR, v = i % VPR;
+        const int p = p0 + r;
+        const int page_id = a.block_table[static_cast<int64_t>(slot) * a.max_pages + p / a.page];
+        const int64_t off = ((static_cast<int64_t>(page_id) * a.hkv + kvh) * a.page + p % a.page) * HD;
+        reinterpret_cast<int4*>(sK + r * HD)[v] = reinterpret_cast<const int4*>(a.kcache + off)[v];
+        reinterpret_cast<int4*>(sV + r * HD)[v] = reinterpret_cast<const int4*>(a.vcache + off)[v];
+    }
+    __syncthreads();
+
+    for (int p = warp; p < n; p += 4) {
+        float kv[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) kv[j] = bf2f(sK[p * HD + lane * E + j]);
+        for (int g = 0; g < G; ++g) {
+            float pr[E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) pr[j] = __fmul_rn(sQ[g * HD + lane * E + j], kv[j]);
+            float s = local_tree_sum<E>(pr);
+            s = warp_tree_sum(s);
+            if (lane == 0) sS[g * CH + p] = __fmul_rn(s, scale);
+        }
+    }
+    __syncthreads();
+
+    for (int g = warp; g < G; g += 4) {
+        float sv[4];
+        float m = -FLT_MAX;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = lane * 4 + j;
+            sv[j] = p < n ? sS[g * CH + p] : 0.0f;
+            if (p < n) m = fmaxf(m, sv[j]);
+        }
+        m = warp_max(m);
+        float e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = lane * 4 + j;
+            e[j] = p < n ? det_expf(__fsub_rn(sv[j], m)) : kNegZero;
+            sS[g * CH + p] = e[j];
+        }
+        float l = local_tree_sum<4>(e);
+        l = warp_tree_sum(l);
+        if (lane == 0) {
+            sM[g] = m;
+            sL[g] = l;
+        }
+    }
+    __syncthreads();
+
+    float* ws = a.ws + ((static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks + c) * G * (HD + 2);
+    for (int idx = tid; idx < G * HD; idx += 128) {
+        const int g = idx / HD, dd = idx % HD;
+        float acc = 0.0f;
+        for (int p = 0; p < n; ++p) acc = __fmaf_rn(sS[g * CH + p], bf2f(sV[p * HD + dd]), acc);
+        ws[g * (HD + 2) + 2 + dd] = acc;
+    }
+    if (tid < G) {
+        ws[tid * (HD + 2)] = sM[tid];
+        ws[tid * (HD + 2) + 1] = sL[tid];
+    }
+}
+
+// out_d = bf16( (sum_c o_cd * a_c) / (sum_c l_c * a_c) ), a_c = exp(m_c - max_c m_c), chunk order.
+template <int HD>
+__global__ void __launch_bounds__(HD) attn_combine_kernel(const AttnParams a) {
+    pdl_trigger();
+    const int h = blockIdx.x, col = blockIdx.y;
+    pdl_wait();
+    const int pos = a.col_pos[col];
+    if (pos < 0) return;
+    const int G = a.hq / a.hkv;
+    const int kvh = h / G, g = h % G;
+    const int nch = (pos + kAttnChunk) / kAttnChunk;
+    const float* base = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2) + g * (HD + 2);
+    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
+    float M = -FLT_MAX;
+    for (int c = 0; c < nch; ++c) M = fmaxf(M, base[c * cstride]);
+    float L = 0.0f, O = 0.0f;
+    const int d = threadIdx.x;
+    for (int c = 0; c < nch; ++c) {
+        const float* w = base + c * cstride;
+        const float al = det_expf(__fsub_rn(w[0], M));
+        L = __fmaf_rn(w[1], al, L);
+        O = __fmaf_rn(w[2 + d], al, O);
+    }
+    a.out[static_cast<int64_t>(col) * a.hq * HD + h * HD + d] = f2bf(__fdiv_rn(O, L));
+}
+
+// ------------------------------------------------------------------ softmax + decode
+// reference: det_softmax (detcore.cpp:187-198), decode_with_draw / decode_step (detcore.cpp:202-262)
+__device__ __forceinline__ uint64_t prob_key(float p, int idx) {
+    return (static_cast<uint64_t>(__float_as_uint(p)) << 32) | static_cast<uint32_t>(0xFFFFFFFFu - idx);
+}
+__device__ __forceinline__ float key_prob(uint64_t k) { return __uint_as_float(static_cast<uint32_t>(k >> 32)); }
+__device__ __forceinline__ int key_idx(uint64_t k) { return static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(k)); }
+
+struct SampleSmem {
+    float tiles[1024];
+    uint64_t sort[1024];
+    unsigned int hist[256];
+    float red_f[32];
+    int red_i[32];
+    unsigned int count;
+    int flag;
+    float fval;
+    uint64_t kval;
+};
+
+__global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
+    __shared__ SampleSmem sm;
+    pdl_trigger();
+    pdl_wait();
+    const int r = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int slot = r, step = 0;
+    if (sp.col_step != nullptr) {
+        step = sp.col_step[r];
+        if (step < 0) return;
+        slot = sp.col_slot[r];
+    }
+    const DevPolicy pol = sp.policy[slot];
+    const int V = sp.vocab;
+    const float* L = sp.col_step != nullptr
+                         ? sp.logits + static_cast<int64_t>(slot) * sp.slot_stride + static_cast<int64_t>(step) * V
+                         : sp.logits + static_cast<int64_t>(r) * sp.logit_row_stride;
+    float* P = sp.probs + static_cast<int64_t>(r) * V;
+    uint64_t* sorted = sp.scratch + static_cast<int64_t>(r) * V;
+
+    // pass 1: max (left scan order is irrelevant for max) + finiteness (detcore.cpp:127-133)
+    float m = -FLT_MAX;
+    int bad = 0;
+    for (int i = tid; i < V; i += 1024) {
+        const float v = L[i];
+        if (!isfinite(v)) bad = 1;
+        m = fmaxf(m, v);
+    }
+    m = warp_max(m);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        sm.red_f[warp] = m;
+        sm.red_i[warp] = bad;
+    }
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+    if (warp == 0) {
+        float mm = sm.red_f[lane];
+        int bb = sm.red_i[lane];
+        mm = warp_max(mm);
+        bb = __any_sync(0xffffffffu, bb);
+        if (lane == 0) {
+            sm.fval = mm;
+            sm.flag = bb;
+        }
+    }
+    __syncthreads();
+    const float maxv = sm.fval;
+    // one generator step per token, drawn before the policy branch (detcore.cpp:256-262)
+    float rdraw = 0.0f;
+    if (tid == 0) {
+        uint64_t* st = sp.prng + static_cast<int64_t>(slot) * 4;
+        uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+        const uint64_t u = xoshiro_next(s);
+        st[0] = s[0];
+        st[1] = s[1];
+        st[2] = s[2];
+        st[3] = s[3];
+        rdraw = __fmul_rn(static_cast<float>(u >> 40), 0x1.0p-24f);
+    }
+    if (sm.flag) {
+        if (tid == 0) {
+            sp.status[slot] = DETGPU_ENONFINITE;
+            sp.token_out[r] = 0;
+            if (sp.col_step_mut != nullptr) {
+                sp.col_step_mut[r] = -1;
+                sp.col_pos[r] = -1;
+            }
+        }
+        return;
+    }
+
+    // pass 2: e_i = exp(l_i - max); S = canonical tree of e
+    const float S = block_tree_sum_1024(
+        V,
+        [&](int i) {
+            const float e = det_expf(__fsub_rn(L[i], maxv));
+            P[i] = e;
+            return e;
+        },
+        sm.tiles);
+    // pass 3: p_i = e_i / S ; argmax with smallest-index tie-break (detcore.cpp:202-208)
+    float bp = -1.0f;
+    int bi = 0x7fffffff;
+    for (int i = tid; i < V; i += 1024) {
+        const float p = __fdiv_rn(P[i], S);
+        P[i] = p;
+        if (p > bp) {
+            bp = p;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (op > bp || (op == bp && oi < bi)) {
+            bp = op;
+            bi = oi;
+        }
+    }
+    __syncthreads();
+    if (lane == 0) {
+        sm.red_f[warp] = bp;
+        sm.red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        bp = sm.red_f[lane];
+        bi = sm.red_i[lane];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (op > bp || (op == bp && oi < bi)) {
+                bp = op;
+                bi = oi;
+            }
+        }
+    }
+    int token = bi;   // valid in thread 0
+    int32_t err = DETGPU_OK;
+
+    if (pol.kind != DETGPU_GREEDY) {
+        __syncthreads();
+        // Candidates in (probability desc, index asc) order, produced 1024 at a time: radix-select
+        // the 1024-th largest key below `upper`, gather, bitonic sort. Thread 0 runs the reference's
+        // sequential cumulative rules over the sorted prefix.
+        uint64_t upper = ~0ull;
+        int consumed = 0;
+        int kept = 0;          // length of the kept prefix once decided
+        bool decided = false;
+        const int target_k = pol.kind == DETGPU_TOP_K ? static_cast<int>(pol.k < static_cast<uint32_t>(V) ? pol.k : static_cast<uint32_t>(V)) : V;
+        float cum = 0.0f;      // nucleus running sum (thread 0)
+        while (!decided) {
+            const int remaining = V - consumed;
+            const int take = min(1024, remaining);
+            uint64_t kappa = 0;
+            if (remaining > 1024) {
+                uint64_t prefix = 0, mask = 0;
+                unsigned int want = 1024;
+                for (int shift = 56; shift >= 0; shift -= 8) {
+                    if (tid < 256) sm.hist[tid] = 0;
+                    __syncthreads();
+                    for (int i = tid; i < V; i += 1024) {
+                        const uint64_t k = prob_key(P[i], i);
+                        if (k < upper && (k & mask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255], 1u);
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        unsigned int acc = 0;
+                        int b = 255;
+                        for (; b > 0; --b) {
+                            if (acc + sm.hist[b] >= want) break;
+                            acc += sm.hist[b];
+                        }
+                        sm.kval = static_cast<uint64_t>(b);
+                        sm.count = want - acc;
+                    }
+                    __syncthreads();
+                    prefix |= sm.kval << shift;
+                    mask |= 255ull << shift;
+                    want = sm.count;
+                    __syncthreads();
+                }
+                kappa = prefix;
+            }
+            // gather keys in [kappa, upper)
+            if (tid == 0) sm.count = 0;
+            sm.sort[tid] = 0;
+            __syncthreads();
+            for (int i = tid; i < V; i += 1024) {
+                const uint64_t k = prob_key(P[i], i);
+                if (k < upper && k >= kappa) sm.sort[atomicAdd(&sm.count, 1u)] = k;
+            }
+            __syncthreads();
+            // bitonic sort, descending
+            for (int kk = 2; kk <= 1024; kk <<= 1) {
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    const int ixj = tid ^ j;
+                    if (ixj > tid) {
+                        const uint64_t x = sm.sort[tid], y = sm.sort[ixj];
+                        const bool desc = (tid & kk) == 0;
+                        if (desc ? (x < y) : (x > y)) {
+                            sm.sort[tid] = y;
+                            sm.sort[ixj] = x;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            if (tid == 0) {
+                int dec = 0;
+                for (int j = 0; j < take; ++j) {
+                    const uint64_t k = sm.sort[j];
+                    sorted[consumed + j] = k;
+                    if (dec) continue;
+                    if (pol.kind == DETGPU_TOP_K) {
+                        if (consumed + j + 1 >= target_k) {
+                            kept = target_k;
+                            dec = 1;
+                        }
+                    } else {
+                        cum = __fadd_rn(cum, key_prob(k));
+                        if (cum >= pol.p) {
+                            kept = consumed + j + 1;
+                            dec = 1;
+                        }
+                    }
+                }
+                if (!dec && consumed + take >= V) {
+                    kept = V;
+                    dec = 1;
+                }
+                sm.flag = dec;
+                sm.count = kept;
+                sm.kval = sm.sort[take - 1];
+            }
+            __syncthreads();
+            decided = sm.flag != 0;
+            kept = static_cast<int>(sm.count);
+            upper = sm.kval;
+            consumed += take;
+            __syncthreads();
+        }
+        // renormalise with the canonical tree over the kept prefix, in sorted order
+        const float mass = block_tree_sum_1024(kept, [&](int i) { return key_prob(sorted[i]); }, sm.tiles);
+        if (tid == 0) {
+            if (!(mass > 0.0f)) {
+                err = DETGPU_EINVAL;
+                token = 0;
+            } else {
+                float c2 = 0.0f;
+                token = key_idx(sorted[kept - 1]);   // rounding left cum slightly below r
+                for (int i = 0; i < kept; ++i) {
+                    c2 = __fadd_rn(c2, __fdiv_rn(key_prob(sorted[i]), mass));
+                    if (c2 >= rdraw) {
+                        token = key_idx(sorted[i]);
+                        break;
+                    }
+                }
+            }
+        }
+    }
+
+    if (tid == 0) {
+        sp.token_out[r] = static_cast<uint32_t>(token);
+        if (err != DETGPU_OK) sp.status[slot] = err;
+        if (sp.tokens_hist != nullptr) sp.tokens_hist[static_cast<int64_t>(slot) * sp.tcap + step] = token;
+        if (sp.col_step_mut != nullptr) {
+            if (err != DETGPU_OK || step + 1 >= pol.max_tokens) {
+                sp.col_step_mut[r] = -1;
+                sp.col_pos[r] = -1;
+            } else {
+                sp.col_step_mut[r] = step + 1;
+                sp.col_pos[r] = sp.col_pos[r] + 1;
+            }
+        }
+    }
+}
+
+cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStream_t stream, cudaLaunchAttribute* attr,
+                            bool pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+}  // namespace
+
+cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
+                           const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* col_index, int ncols, int d,
+                           float eps, cudaStream_t stream, bool pdl) {
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = make_cfg(dim3(ncols), dim3(256), 0, stream, attr, pdl);
+    switch (d) {
+        case 256:
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<1>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+        case 512:
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<2>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+        case 1024:
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<4>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+        case 2048:
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<8>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+        case 4096:
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<16>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_expf(const float* x, float* y, int64_t n, cudaStream_t stream) {
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    expf_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree_sum(const float* x, float* out, int rows, int n, cudaStream_t stream) {
+    if (n > 131072 || rows <= 0) return cudaErrorInvalidValue;
+    tree_sum_kernel<<<rows, 1024, 0, stream>>>(x, out, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_tensor(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp,
+                               int is_gamma, int row_mul, int row_add, cudaStream_t stream) {
+    const float scale = ldexpf(1.0f, scale_exp);
+    const int64_t n = rows * cols;
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 32));
+    init_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(dst, seed, rows, cols, scale, is_gamma, row_mul, row_add);
+    return cudaGetLastError();
+}
+
+size_t attn_workspace_bytes(const AttnParams& a) {
+    const int G = a.hq / a.hkv;
+    return sizeof(float) * static_cast<size_t>(a.ncols) * a.hkv * a.max_chunks * G * (a.hd + 2);
+}
+
+cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    if (a.hq % a.hkv != 0 || a.hq / a.hkv > 8) return cudaErrorInvalidValue;
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(a.hd)));
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(attn_chunk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kAttnChunk * 128 * 2);
+        cudaFuncSetAttribute(attn_chunk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kAttnChunk * 64 * 2);
+        attr_set = true;
+    }
+    cudaLaunchAttribute attr[1];
+    const size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * a.hd * 2;
+    cudaLaunchConfig_t c1 = make_cfg(dim3(a.max_chunks, a.hkv, a.ncols), dim3(128), dsm, stream, attr, pdl);
+    cudaError_t e;
+    if (a.hd == 128) e = cudaLaunchKernelEx(&c1, attn_chunk_kernel<128>, a, scale);
+    else if (a.hd == 64) e = cudaLaunchKernelEx(&c1, attn_chunk_kernel<64>, a, scale);
+    else return cudaErrorInvalidValue;
+    if (e != cudaSuccess) return e;
+    cudaLaunchAttribute attr2[1];
+    cudaLaunchConfig_t c2 = make_cfg(dim3(a.hq, a.ncols), dim3(a.hd), 0, stream, attr2, pdl);
+    if (a.hd == 128) return cudaLaunchKernelEx(&c2, attn_combine_kernel<128>, a);
+    return cudaLaunchKernelEx(&c2, attn_combine_kernel<64>, a);
+}
+
+size_t sample_scratch_bytes(int rows, int vocab) { return sizeof(uint64_t) * static_cast<size_t>(rows) * vocab; }
+
+cudaError_t launch_sample(const SampleParams& sp, cudaStream_t stream, bool pdl) {
+    if (sp.vocab > 131072 || sp.vocab <= 0) return cudaErrorInvalidValue;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = make_cfg(dim3(sp.rows), dim3(1024), 0, stream, attr, pdl);
+    return cudaLaunchKernelEx(&cfg, sample_kernel, sp);
+}
+
+}  // namespace detgpu

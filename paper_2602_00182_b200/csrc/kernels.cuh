@@ -1,0 +1,80 @@
+// Non-GEMM kernels of the deterministic decode path (declarations).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "detgpu.h"
+
+namespace detgpu {
+
+// Attention KV chunk: positions [c*kAttnChunk, (c+1)*kAttnChunk) form one online-softmax chunk,
+// combined in chunk order. Part of the numeric definition; never batch-dependent.
+constexpr int kAttnChunk = 128;
+
+// ---- RMSNorm (optionally with the embedding gather fused in) ----
+// x_in [rows][d] f32 (row = col_index ? col_index[col] : col); when embed != nullptr the input row
+// is embed[col_token[col]] (bf16) and is also written to x_out[col][d] as f32.
+cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
+                           const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* col_index, int ncols, int d,
+                           float eps, cudaStream_t stream, bool pdl);
+
+cudaError_t launch_expf(const float* x, float* y, int64_t n, cudaStream_t stream);
+cudaError_t launch_tree_sum(const float* x, float* out, int rows, int n, cudaStream_t stream);
+cudaError_t launch_init_tensor(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp,
+                               int is_gamma, int row_mul, int row_add, cudaStream_t stream);
+
+// ---- attention ----
+struct AttnParams {
+    const __nv_bfloat16* q;        // [ncols][hq*hd]
+    const __nv_bfloat16* kcache;   // [pages][hkv][page][hd]
+    const __nv_bfloat16* vcache;
+    const int* block_table;        // [slots][max_pages]
+    const int* col_pos;            // query position (<0 inactive); attends to [0, pos]
+    const int* col_req;            // slot of each column
+    __nv_bfloat16* out;            // [ncols][hq*hd]
+    float* ws;                     // partials
+    int ncols, hq, hkv, hd, page, max_pages, max_chunks;
+};
+size_t attn_workspace_bytes(const AttnParams& a);
+cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);
+
+// ---- softmax + decode ----
+struct DevPolicy {
+    int kind;        // DETGPU_GREEDY / TOP_K / NUCLEUS
+    uint32_t k;
+    float p;
+    int max_tokens;
+};
+inline DevPolicy to_dev_policy(const detgpu_policy& p) {
+    DevPolicy d;
+    d.kind = p.kind;
+    d.k = p.has_k ? p.k : 0;
+    d.p = p.has_p ? p.p : 0.0f;
+    d.max_tokens = static_cast<int>(p.max_tokens);
+    return d;
+}
+
+struct SampleParams {
+    const float* logits;        // row r at logits + row_off(r)
+    int64_t logit_row_stride;   // used when col_step == nullptr
+    const int* col_step;        // engine: trace step of each row (<0 inactive)
+    const int* col_slot;
+    int64_t slot_stride;
+    int rows, vocab;
+    const DevPolicy* policy;    // per row (engine: per slot via col_slot)
+    uint64_t* prng;             // [slot][4]
+    float* probs;               // [rows][vocab] scratch / output
+    uint64_t* scratch;          // sample_scratch_bytes
+    uint32_t* token_out;        // [rows] (engine: next input token)
+    int32_t* status;            // [rows] (or per slot)
+    // engine bookkeeping (nullable): tokens_hist[slot*tcap + step] = token; pos/step advance
+    uint32_t* tokens_hist;
+    int tcap;
+    int* col_pos;
+    int* col_step_mut;
+};
+size_t sample_scratch_bytes(int rows, int vocab);
+cudaError_t launch_sample(const SampleParams& sp, cudaStream_t stream, bool pdl);
+
+}  // namespace detgpu

@@ -1,0 +1,75 @@
+"""tcgen05 GEMM: numerics against an fp64 torch reference, and batch invariance (bitwise).
+
+The reduction order inside one tcgen05.mma (K=16) is hardware-defined, so the GEMM is checked
+against fp64 within a bound derived from the magnitudes; everything that decides bits on our side
+(K order, tile shape, sub-tile position) is checked bitwise across batch sizes and permutations.
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(W, X, n_out=None):
+    import torch
+    from paper_2602_00182_b200._lib import lib, check
+
+    n_out = W.shape[0] if n_out is None else n_out
+    Y = torch.full((X.shape[0], n_out), float("nan"), dtype=torch.float32, device=W.device)
+    check(lib.detgpu_k_gemm(W.data_ptr(), X.data_ptr(), Y.data_ptr(), n_out, W.shape[1], X.shape[0], n_out, None))
+    torch.cuda.synchronize()
+    return Y
+
+
+def _rand_bf16(shape, gen, scale=1.0):
+    import torch
+
+    return (torch.rand(shape, generator=gen, dtype=torch.float32) * 2 - 1).mul(scale).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("n_out,K,ncols", [(128, 64, 1), (256, 256, 8), (384, 512, 64), (512, 1024, 100),
+                                            (256, 4096, 256), (128, 768, 300), (1024, 256, 513)])
+def test_gemm_matches_fp64(n_out, K, ncols):
+    import torch
+
+    g = torch.Generator().manual_seed(n_out * 7 + K + ncols)
+    W = _rand_bf16((n_out, K), g)
+    X = _rand_bf16((ncols, K), g)
+    Y = _gemm(W, X)
+    ref = X.double() @ W.double().T
+    bound = (X.double().abs() @ W.double().abs().T) * (K * 2.0 ** -23) + 1e-30
+    err = (Y.double() - ref).abs()
+    assert torch.isfinite(Y).all()
+    assert (err <= bound).all(), f"max err {err.max().item()} bound {bound.min().item()}"
+
+
+def test_batch_invariance_bitwise():
+    import torch
+
+    g = torch.Generator().manual_seed(1234)
+    W = _rand_bf16((512, 1024), g, 0.05)
+    X = _rand_bf16((300, 1024), g)
+    full = _gemm(W, X)
+    for n in (1, 2, 7, 63, 64, 65, 128, 129, 255, 256, 257):
+        part = _gemm(W, X[:n].contiguous())
+        assert torch.equal(part.view(torch.int32), full[:n].view(torch.int32)), f"ncols={n}"
+    perm = torch.randperm(300, generator=g)
+    permuted = _gemm(W, X[perm.cuda()].contiguous())
+    assert torch.equal(permuted.view(torch.int32), full[perm.cuda()].view(torch.int32))
+    # single column at every sub-tile position of a 256-wide tile
+    col = X[5:6]
+    for pos in (0, 1, 31, 63, 64, 127, 200, 255):
+        Xp = X[:256].clone()
+        Xp[pos] = col[0]
+        Yp = _gemm(W, Xp)
+        assert torch.equal(Yp[pos].view(torch.int32), full[5].view(torch.int32)), f"pos={pos}"
+
+
+def test_repeat_bitwise():
+    import torch
+
+    g = torch.Generator().manual_seed(99)
+    W = _rand_bf16((1024, 4096), g, 0.02)
+    X = _rand_bf16((16, 4096), g)
+    first = _gemm(W, X)
+    for _ in range(20):
+        assert torch.equal(_gemm(W, X).view(torch.int32), first.view(torch.int32))
