@@ -115,6 +115,15 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
                     uint32_t batch_size, uint32_t* const* tokens_out, float* const* logits_out,
                     uint8_t* out_hash, uint32_t flags, detgpu_stats* stats);
 
+/* The engine's CUDA stream (so callers can bracket work with their own events). */
+void* detgpu_stream(const detgpu_engine* h);
+/* One un-graphed decode step (forward + lm_head + sample) for ncols slots at context ctx with an
+ * event after every launch: mean ms per step by kernel class (0 norm, 1 qkv, 2 attention, 3 o,
+ * 4 gate/up, 5 down, 6 lm_head, 7 sample) and launches per step by class. Measurement hook for
+ * bench.py's roofline; never used on the serving path. */
+int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t reps,
+                               float* ms_by_class, uint32_t* launches_by_class);
+
 /* ---- host-side helpers of the receipt path (no GPU needed) ---- */
 
 /* SHA-256 (receipts.hpp:53-54 hash_commit; sha256.cpp:32-37). */

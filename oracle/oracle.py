@@ -28,6 +28,8 @@ def lib():
         vp, sz, u32, u64, i32, i64, f32 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64, C.c_int, C.c_int64, C.c_float
         sig = {
             "orc_set_threads": (None, [i32]), "orc_get_threads": (i32, []),
+            "orc_set_gemm_mode": (None, [i32]), "orc_tc_dot": (f32, [vp, vp, i32]),
+            "orc_gemm": (None, [vp, vp, i32, i32, i32, vp]),
             "orc_fnv1a64": (u64, [C.c_char_p]), "orc_mix_seed": (u64, [u64, u64]),
             "orc_prng_seeded": (None, [u64, vp]), "orc_prng_next_u64": (u64, [vp]),
             "orc_prng_next_below": (u64, [vp, u64]), "orc_prng_next_unit_f32": (f32, [vp]),
@@ -180,6 +182,28 @@ def toy_infer(model_id: str, arch: str, prompt, kind: int, k=None, p=None, max_t
     if rc != 0:
         raise ValueError(f"toy infer failed ({rc})")
     return toks[:max_tokens].copy(), logits[:max_tokens].copy()
+
+
+def gemm(W_u16: np.ndarray, X_u16: np.ndarray) -> np.ndarray:
+    """Y[c, r] = W[r] . X[c] under the active accumulation profile (default: b200 / tcgen05)."""
+    W = np.ascontiguousarray(W_u16, dtype=np.uint16)
+    X = np.ascontiguousarray(X_u16, dtype=np.uint16)
+    Y = np.zeros((X.shape[0], W.shape[0]), dtype=np.float32)
+    lib().orc_gemm(ptr(W), ptr(X), W.shape[0], W.shape[1], X.shape[0], ptr(Y))
+    return Y
+
+
+class gemm_profile:
+    """Context manager: 0 = b200 (tcgen05 accumulation), 1 = reference canonical tree (archA-style)."""
+
+    def __init__(self, mode: int):
+        self.mode = mode
+
+    def __enter__(self):
+        lib().orc_set_gemm_mode(self.mode)
+
+    def __exit__(self, *a):
+        lib().orc_set_gemm_mode(0)
 
 
 def gen_tensor(seed: int, rows: int, cols: int, scale_exp: int, is_gamma: bool) -> np.ndarray:

@@ -1,0 +1,855 @@
+// The deterministic inference engine: weights, paged KV cache, prefill + decode loop (CUDA graph
+// per batch size), host receipt hashing, and the engine part of the C-ABI (include/detgpu.h).
+//
+// Reference path replaced: detcore::infer / infer_batch (reference proj/src/detcore.cpp:319-410)
+// and out_hash = SHA-256(canonical_bytes) (proj/src/receipts.cpp:120). One engine = one GPU
+// replica; requests of a generate() call are decoded in groups of batch_size with per-request
+// state (prng, position, trace step) living in device memory.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.h"
+#include "detgpu.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "model.h"
+#include "receipt.h"
+#include "toy.cuh"
+
+namespace detgpu {
+
+namespace {
+
+constexpr int kPage = 64;          // KV positions per page
+constexpr int kPrefillCols = 2048; // max activation columns per forward pass
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(count, 1));
+}
+
+struct Layer {
+    __nv_bfloat16 *attn_norm = nullptr, *wqkv = nullptr, *wo = nullptr, *ffn_norm = nullptr, *wgu = nullptr,
+                  *wdown = nullptr;
+    CUtensorMap tm_qkv, tm_o, tm_gu, tm_down;
+};
+
+}  // namespace
+
+struct Engine {
+    int device = 0;
+    std::string model_id, arch;
+    ModelConfig cfg{};
+    bool toy = false;
+    uint32_t max_batch = 0, max_context = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    std::vector<void*> allocs;
+
+    // weights
+    __nv_bfloat16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+    CUtensorMap tm_lm;
+    std::vector<Layer> layers;
+    uint64_t n_params = 0;
+    // activations
+    int col_cap = 0;
+    float* x = nullptr;
+    __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *h_last = nullptr;
+    CUtensorMap tm_h, tm_attn, tm_act, tm_hlast;
+    // KV cache (paged, static page ownership per slot)
+    __nv_bfloat16 *kpool = nullptr, *vpool = nullptr;
+    int pages_per_slot = 0, total_pages = 0, max_chunks = 0;
+    int* block_table = nullptr;
+    float* attn_ws = nullptr;
+    float *rope_cos = nullptr, *rope_sin = nullptr;
+    // prefill plan
+    int *p_tok = nullptr, *p_pos = nullptr, *p_req = nullptr, *p_last_in = nullptr, *p_last_out = nullptr;
+    // per-slot decode state
+    int *d_tok = nullptr, *d_pos = nullptr, *d_req = nullptr, *d_step = nullptr, *d_status = nullptr;
+    uint64_t* d_prng = nullptr;
+    DevPolicy* d_pol = nullptr;
+    float* probs = nullptr;
+    uint64_t* sort_scratch = nullptr;
+    // outputs (grown on demand)
+    float* trace = nullptr;
+    size_t trace_cap = 0;
+    uint32_t* tok_hist = nullptr;
+    size_t tok_cap = 0;
+    int64_t slot_stride = 0;
+    int tcap = 0;
+    // pinned staging for D2H
+    float* pinned[2] = {nullptr, nullptr};
+    size_t pinned_floats = 0;
+    // decode graphs keyed by (ncols, slot_stride)
+    std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
+    uint64_t launches_per_step = 0;
+    bool use_pdl = true;
+    // toy model
+    ToyWeights toyw{};
+
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<std::pair<cudaEvent_t, int>>* prof = nullptr;
+
+    template <class T>
+    cudaError_t alloc(T** p, size_t count) {
+        cudaError_t e = dalloc(p, count);
+        if (e == cudaSuccess) allocs.push_back(*p);
+        return e;
+    }
+    ~Engine() {
+        cudaSetDevice(device);
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+        for (void* p : allocs) cudaFree(p);
+        if (trace) cudaFree(trace);
+        if (tok_hist) cudaFree(tok_hist);
+        for (float* p : pinned)
+            if (p) cudaFreeHost(p);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        toy_free(toyw);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+int fail(Engine* e, int code, const std::string& msg) {
+    if (e) e->err = msg;
+    set_global_error(msg);
+    return code;
+}
+
+#define ENG_CUDA(expr)                                                                                 \
+    do {                                                                                               \
+        cudaError_t _e = (expr);                                                                       \
+        if (_e != cudaSuccess) return fail(E, DETGPU_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+int init_weights(Engine* E) {
+    const ModelConfig& c = E->cfg;
+    const int d = c.d, qd = c.hq * c.hd, kd = c.hkv * c.hd, F = c.F, V = c.V;
+    const int sd = -half_log2_round(d), sq = -half_log2_round(qd), sf = -half_log2_round(F);
+    const uint64_t base = fnv1a64(E->model_id.c_str());
+    auto seed = [&](int tid) { return mix_seed(base, static_cast<uint64_t>(tid)); };
+    cudaStream_t s = E->stream;
+    ENG_CUDA(E->alloc(&E->embed, size_t(V) * d));
+    ENG_CUDA(E->alloc(&E->lm_head, size_t(V) * d));
+    ENG_CUDA(E->alloc(&E->final_norm, d));
+    ENG_CUDA(launch_init_tensor(E->embed, seed(0), V, d, 0, 0, 1, 0, s));
+    ENG_CUDA(launch_init_tensor(E->lm_head, seed(1), V, d, 4 + sd, 0, 1, 0, s));
+    ENG_CUDA(launch_init_tensor(E->final_norm, seed(2), 1, d, 0, 1, 1, 0, s));
+    if (!make_tmap_bf16(&E->tm_lm, E->lm_head, d, V, 128)) return fail(E, DETGPU_ECUDA, "tensor map (lm_head)");
+    E->n_params = 2ull * V * d + d;
+    E->layers.resize(c.L);
+    for (int l = 0; l < c.L; ++l) {
+        Layer& Ly = E->layers[l];
+        ENG_CUDA(E->alloc(&Ly.attn_norm, d));
+        ENG_CUDA(E->alloc(&Ly.ffn_norm, d));
+        ENG_CUDA(E->alloc(&Ly.wqkv, size_t(qd + 2 * kd) * d));
+        ENG_CUDA(E->alloc(&Ly.wo, size_t(d) * qd));
+        ENG_CUDA(E->alloc(&Ly.wgu, size_t(2 * F) * d));
+        ENG_CUDA(E->alloc(&Ly.wdown, size_t(d) * F));
+        ENG_CUDA(launch_init_tensor(Ly.attn_norm, seed(layer_tensor_id(l, kAttnNorm)), 1, d, 0, 1, 1, 0, s));
+        ENG_CUDA(launch_init_tensor(Ly.ffn_norm, seed(layer_tensor_id(l, kFfnNorm)), 1, d, 0, 1, 1, 0, s));
+        // fused QKV rows: [wq ; wk ; wv]
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWq)), qd, d, sd, 0, 1, 0, s));
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWk)), kd, d, sd, 0, 1, qd, s));
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWv)), kd, d, sd, 0, 1, qd + kd, s));
+        ENG_CUDA(launch_init_tensor(Ly.wo, seed(layer_tensor_id(l, kWo)), d, qd, sq, 0, 1, 0, s));
+        // gate/up interleaved by row: physical 2j = gate j, 2j+1 = up j (SwiGLU epilogue pairs)
+        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWgate)), F, d, sd, 0, 2, 0, s));
+        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWup)), F, d, sd, 0, 2, 1, s));
+        ENG_CUDA(launch_init_tensor(Ly.wdown, seed(layer_tensor_id(l, kWdown)), d, F, sf, 0, 1, 0, s));
+        if (!make_tmap_bf16(&Ly.tm_qkv, Ly.wqkv, d, qd + 2 * kd, 128) || !make_tmap_bf16(&Ly.tm_o, Ly.wo, qd, d, 128) ||
+            !make_tmap_bf16(&Ly.tm_gu, Ly.wgu, d, 2 * F, 128) || !make_tmap_bf16(&Ly.tm_down, Ly.wdown, F, d, 128))
+            return fail(E, DETGPU_ECUDA, "tensor map (layer)");
+        E->n_params += 2ull * d + size_t(qd + 2 * kd) * d + size_t(d) * qd + 3ull * F * d;
+    }
+    return DETGPU_OK;
+}
+
+int init_buffers(Engine* E) {
+    const ModelConfig& c = E->cfg;
+    const int d = c.d, qd = c.hq * c.hd, kd = c.hkv * c.hd;
+    const int B = static_cast<int>(E->max_batch);
+    E->col_cap = std::max(B, kPrefillCols);
+    const int C = E->col_cap;
+    ENG_CUDA(E->alloc(&E->x, size_t(C) * d));
+    ENG_CUDA(E->alloc(&E->h, size_t(C) * d));
+    ENG_CUDA(E->alloc(&E->q, size_t(C) * qd));
+    ENG_CUDA(E->alloc(&E->attn, size_t(C) * qd));
+    ENG_CUDA(E->alloc(&E->act, size_t(C) * c.F));
+    ENG_CUDA(E->alloc(&E->h_last, size_t(B) * d));
+    ENG_CUDA(cudaMemsetAsync(E->h, 0, sizeof(__nv_bfloat16) * size_t(C) * d, E->stream));
+    ENG_CUDA(cudaMemsetAsync(E->attn, 0, sizeof(__nv_bfloat16) * size_t(C) * qd, E->stream));
+    ENG_CUDA(cudaMemsetAsync(E->act, 0, sizeof(__nv_bfloat16) * size_t(C) * c.F, E->stream));
+    ENG_CUDA(cudaMemsetAsync(E->h_last, 0, sizeof(__nv_bfloat16) * size_t(B) * d, E->stream));
+    if (!make_tmap_bf16(&E->tm_h, E->h, d, C, 64) || !make_tmap_bf16(&E->tm_attn, E->attn, qd, C, 64) ||
+        !make_tmap_bf16(&E->tm_act, E->act, c.F, C, 64) || !make_tmap_bf16(&E->tm_hlast, E->h_last, d, B, 64))
+        return fail(E, DETGPU_ECUDA, "tensor map (activations)");
+    // KV pool: static page ownership, slot b owns pages [b*pps, (b+1)*pps)
+    E->pages_per_slot = (static_cast<int>(E->max_context) + kPage - 1) / kPage;
+    E->total_pages = E->pages_per_slot * B;
+    E->max_chunks = (E->pages_per_slot * kPage + kAttnChunk - 1) / kAttnChunk;
+    const size_t per_layer = size_t(E->total_pages) * kPage * kd;
+    ENG_CUDA(E->alloc(&E->kpool, per_layer * c.L));
+    ENG_CUDA(E->alloc(&E->vpool, per_layer * c.L));
+    std::vector<int> bt(size_t(B) * E->pages_per_slot);
+    for (size_t i = 0; i < bt.size(); ++i) bt[i] = static_cast<int>(i);
+    ENG_CUDA(E->alloc(&E->block_table, bt.size()));
+    ENG_CUDA(cudaMemcpy(E->block_table, bt.data(), sizeof(int) * bt.size(), cudaMemcpyHostToDevice));
+    {
+        AttnParams a{};
+        a.ncols = C;
+        a.hq = c.hq;
+        a.hkv = c.hkv;
+        a.hd = c.hd;
+        a.max_chunks = E->max_chunks;
+        ENG_CUDA(E->alloc(&E->attn_ws, attn_workspace_bytes(a) / sizeof(float)));
+    }
+    // RoPE tables, host binary64 -> f32; identical expression in the oracle.
+    const int npos = static_cast<int>(E->max_context), h2 = c.hd / 2;
+    std::vector<float> cs(size_t(npos) * h2), sn(size_t(npos) * h2);
+    for (int p = 0; p < npos; ++p)
+        for (int i = 0; i < h2; ++i) {
+            const double inv = std::pow(c.theta, -2.0 * i / c.hd);
+            const double ang = double(p) * inv;
+            cs[size_t(p) * h2 + i] = static_cast<float>(std::cos(ang));
+            sn[size_t(p) * h2 + i] = static_cast<float>(std::sin(ang));
+        }
+    ENG_CUDA(E->alloc(&E->rope_cos, cs.size()));
+    ENG_CUDA(E->alloc(&E->rope_sin, sn.size()));
+    ENG_CUDA(cudaMemcpy(E->rope_cos, cs.data(), sizeof(float) * cs.size(), cudaMemcpyHostToDevice));
+    ENG_CUDA(cudaMemcpy(E->rope_sin, sn.data(), sizeof(float) * sn.size(), cudaMemcpyHostToDevice));
+    ENG_CUDA(E->alloc(&E->p_tok, C));
+    ENG_CUDA(E->alloc(&E->p_pos, C));
+    ENG_CUDA(E->alloc(&E->p_req, C));
+    ENG_CUDA(E->alloc(&E->p_last_in, B));
+    ENG_CUDA(E->alloc(&E->p_last_out, B));
+    ENG_CUDA(E->alloc(&E->d_tok, B));
+    ENG_CUDA(E->alloc(&E->d_pos, B));
+    ENG_CUDA(E->alloc(&E->d_req, B));
+    ENG_CUDA(E->alloc(&E->d_step, B));
+    ENG_CUDA(E->alloc(&E->d_status, B));
+    ENG_CUDA(E->alloc(&E->d_prng, size_t(B) * 4));
+    ENG_CUDA(E->alloc(&E->d_pol, B));
+    ENG_CUDA(E->alloc(&E->probs, size_t(B) * c.V));
+    ENG_CUDA(E->alloc(&E->sort_scratch, size_t(B) * c.V));
+    std::vector<int> ident(B);
+    for (int i = 0; i < B; ++i) ident[i] = i;
+    ENG_CUDA(cudaMemcpy(E->d_req, ident.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+    return DETGPU_OK;
+}
+
+// ------------------------------------------------------------------ forward pass
+// Optional per-launch event trail (detgpu_profile_decode_step): kernel classes below.
+enum ProfClass { kProfNorm = 0, kProfQkv, kProfAttn, kProfO, kProfGateUp, kProfDown, kProfLmHead, kProfSample, kProfN };
+void mark(Engine* E, int cls) {
+    if (E->prof == nullptr) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, E->stream);
+    E->prof->push_back({ev, cls});
+}
+GemmParams gemm_base(int n_out, int k, int ncols) {
+    GemmParams p{};
+    p.n_out = n_out;
+    p.k = k;
+    p.ncols = ncols;
+    return p;
+}
+
+// All layers for `ncols` columns. Input: tokens/pos/req per column. Output: x (residual) and, when
+// `final_all`, h = final_norm(x) for all columns; else h_last[out_idx[i]] = final_norm(x[in_idx[i]])
+// for n_last gathered columns.
+cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const int* req, bool final_all,
+                    int n_last, uint64_t* nlaunch) {
+    const ModelConfig& c = E->cfg;
+    const int d = c.d, qd = c.hq * c.hd, kd = c.hkv * c.hd;
+    cudaStream_t s = E->stream;
+    const bool pdl = E->use_pdl;
+    const size_t per_layer = size_t(E->total_pages) * kPage * kd;
+    cudaError_t e;
+    uint64_t n = 0;
+    e = launch_rmsnorm(nullptr, E->x, E->embed, tok, E->layers[0].attn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl);
+    if (e != cudaSuccess) return e;
+    mark(E, kProfNorm);
+    ++n;
+    for (int l = 0; l < c.L; ++l) {
+        const Layer& Ly = E->layers[l];
+        GemmParams g = gemm_base(qd + 2 * kd, d, ncols);
+        g.mode = kEpiQkvRope;
+        g.q_out = E->q;
+        g.hq = c.hq;
+        g.hkv = c.hkv;
+        g.hd = c.hd;
+        g.col_pos = pos;
+        g.col_req = req;
+        g.rope_cos = E->rope_cos;
+        g.rope_sin = E->rope_sin;
+        g.kcache = E->kpool + per_layer * l;
+        g.vcache = E->vpool + per_layer * l;
+        g.block_table = E->block_table;
+        g.max_pages = E->pages_per_slot;
+        g.page = kPage;
+        if ((e = gemm_launch(Ly.tm_qkv, E->tm_h, g, s, pdl)) != cudaSuccess) return e;
+        mark(E, kProfQkv);
+        AttnParams a{};
+        a.q = E->q;
+        a.kcache = E->kpool + per_layer * l;
+        a.vcache = E->vpool + per_layer * l;
+        a.block_table = E->block_table;
+        a.col_pos = pos;
+        a.col_req = req;
+        a.out = E->attn;
+        a.ws = E->attn_ws;
+        a.ncols = ncols;
+        a.hq = c.hq;
+        a.hkv = c.hkv;
+        a.hd = c.hd;
+        a.page = kPage;
+        a.max_pages = E->pages_per_slot;
+        a.max_chunks = E->max_chunks;
+        if ((e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
+        mark(E, kProfAttn);
+        GemmParams go = gemm_base(d, qd, ncols);
+        go.mode = kEpiAddF32;
+        go.out = E->x;
+        go.ld_out = d;
+        if ((e = gemm_launch(Ly.tm_o, E->tm_attn, go, s, pdl)) != cudaSuccess) return e;
+        mark(E, kProfO);
+        if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl)) !=
+            cudaSuccess)
+            return e;
+        mark(E, kProfNorm);
+        GemmParams gu = gemm_base(2 * c.F, d, ncols);
+        gu.mode = kEpiSwiglu;
+        gu.act = E->act;
+        if ((e = gemm_launch(Ly.tm_gu, E->tm_h, gu, s, pdl)) != cudaSuccess) return e;
+        mark(E, kProfGateUp);
+        GemmParams gd = gemm_base(d, c.F, ncols);
+        gd.mode = kEpiAddF32;
+        gd.out = E->x;
+        gd.ld_out = d;
+        if ((e = gemm_launch(Ly.tm_down, E->tm_act, gd, s, pdl)) != cudaSuccess) return e;
+        mark(E, kProfDown);
+        n += 7;
+        if (l + 1 < c.L) {
+            e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, E->layers[l + 1].attn_norm, E->h, nullptr, ncols, d,
+                               c.eps, s, pdl);
+            ++n;
+        } else if (final_all) {
+            e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, E->final_norm, E->h, nullptr, ncols, d, c.eps, s, pdl);
+            ++n;
+        } else if (n_last > 0) {
+            e = launch_rmsnorm_gather(E->x, E->final_norm, E->h_last, E->p_last_in, E->p_last_out, n_last, d, c.eps, s,
+                                      pdl);
+            ++n;
+        }
+        if (e != cudaSuccess) return e;
+        mark(E, kProfNorm);
+    }
+    if (nlaunch) *nlaunch += n;
+    return cudaSuccess;
+}
+
+// lm_head over `ncols` columns of X (tmX) into the trace at (slot, d_step[col]), then the sampler.
+cudaError_t head_and_sample(Engine* E, const CUtensorMap& tmX, int ncols, uint64_t* nlaunch) {
+    const ModelConfig& c = E->cfg;
+    GemmParams g = gemm_base(c.V, c.d, ncols);
+    g.mode = kEpiStoreF32;
+    g.out = E->trace;
+    g.col_step = E->d_step;
+    g.col_slot = E->d_req;
+    g.slot_stride = E->slot_stride;
+    cudaError_t e = gemm_launch(E->tm_lm, tmX, g, E->stream, E->use_pdl);
+    if (e != cudaSuccess) return e;
+    mark(E, kProfLmHead);
+    SampleParams sp{};
+    sp.logits = E->trace;
+    sp.col_step = E->d_step;
+    sp.col_slot = E->d_req;
+    sp.slot_stride = E->slot_stride;
+    sp.rows = ncols;
+    sp.vocab = c.V;
+    sp.policy = E->d_pol;
+    sp.prng = E->d_prng;
+    sp.probs = E->probs;
+    sp.scratch = E->sort_scratch;
+    sp.token_out = reinterpret_cast<uint32_t*>(E->d_tok);
+    sp.status = E->d_status;
+    sp.tokens_hist = E->tok_hist;
+    sp.tcap = E->tcap;
+    sp.col_pos = E->d_pos;
+    sp.col_step_mut = E->d_step;
+    e = launch_sample(sp, E->stream, E->use_pdl);
+    mark(E, kProfSample);
+    if (nlaunch) *nlaunch += 2;
+    return e;
+}
+
+int ensure_outputs(Engine* E, int nslots, int tmax) {
+    const size_t need_trace = size_t(nslots) * tmax * E->cfg.V;
+    if (need_trace > E->trace_cap) {
+        if (E->trace) cudaFree(E->trace);
+        E->trace = nullptr;
+        ENG_CUDA(dalloc(&E->trace, need_trace));
+        E->trace_cap = need_trace;
+        for (auto& gph : E->graphs) cudaGraphExecDestroy(gph.second);
+        E->graphs.clear();
+    }
+    const size_t need_tok = size_t(nslots) * tmax;
+    if (need_tok > E->tok_cap) {
+        if (E->tok_hist) cudaFree(E->tok_hist);
+        E->tok_hist = nullptr;
+        ENG_CUDA(dalloc(&E->tok_hist, need_tok));
+        E->tok_cap = need_tok;
+        for (auto& gph : E->graphs) cudaGraphExecDestroy(gph.second);
+        E->graphs.clear();
+    }
+    if (E->tcap != tmax || E->slot_stride != int64_t(tmax) * E->cfg.V) {
+        E->tcap = tmax;
+        E->slot_stride = int64_t(tmax) * E->cfg.V;
+    }
+    return DETGPU_OK;
+}
+
+int get_graph(Engine* E, int ncols, cudaGraphExec_t* out) {
+    auto key = std::make_pair(ncols, E->slot_stride);
+    auto it = E->graphs.find(key);
+    if (it != E->graphs.end()) {
+        *out = it->second;
+        return DETGPU_OK;
+    }
+    cudaGraph_t g;
+    ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+    uint64_t n = 0;
+    cudaError_t e = forward(E, ncols, E->d_tok, E->d_pos, E->d_req, true, 0, &n);
+    if (e == cudaSuccess) e = head_and_sample(E, E->tm_h, ncols, &n);
+    cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
+    ENG_CUDA(e);
+    ENG_CUDA(e2);
+    cudaGraphExec_t ex;
+    ENG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    E->graphs[key] = ex;
+    E->launches_per_step = n;
+    *out = ex;
+    return DETGPU_OK;
+}
+
+std::string validate_policy(const detgpu_policy& p) {
+    // DecodePolicy::validate (detcore.cpp:52-69)
+    switch (p.kind) {
+        case DETGPU_GREEDY:
+            if (p.has_k || p.has_p) return "greedy policy must not carry k or p";
+            return "";
+        case DETGPU_TOP_K:
+            if (!p.has_k) return "top_k policy requires k";
+            if (p.k == 0) return "top_k k must be positive";
+            if (p.has_p) return "top_k policy must not carry p";
+            return "";
+        case DETGPU_NUCLEUS:
+            if (!p.has_p) return "nucleus policy requires p";
+            if (!(p.p > 0.0f) || p.p > 1.0f) return "nucleus p must be in (0,1]";
+            if (p.has_k) return "nucleus policy must not carry k";
+            return "";
+        default:
+            return "unknown decode kind";
+    }
+}
+
+struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double ms() const {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+// One group of n <= max_batch requests through prefill + decode; results left in trace/tok_hist.
+int run_group(Engine* E, uint32_t n, const uint32_t* const* prompts, const uint32_t* lens, const detgpu_policy* pols,
+              const uint64_t* seeds, detgpu_stats* st) {
+    const ModelConfig& c = E->cfg;
+    cudaStream_t s = E->stream;
+    int tmax = 0;
+    for (uint32_t i = 0; i < n; ++i) tmax = std::max<int>(tmax, static_cast<int>(pols[i].max_tokens));
+    if (tmax == 0) return DETGPU_OK;
+    if (int rc = ensure_outputs(E, static_cast<int>(n), tmax)) return rc;
+    // per-slot state
+    std::vector<int> step(n), pos(n), zero(n, 0);
+    std::vector<uint64_t> prng(size_t(n) * 4);
+    std::vector<DevPolicy> dp(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        const bool active = pols[i].max_tokens > 0;
+        step[i] = active ? 0 : -1;
+        pos[i] = active ? static_cast<int>(lens[i]) - 1 : -1;
+        prng_seeded(seeds[i], &prng[size_t(i) * 4]);
+        dp[i] = to_dev_policy(pols[i]);
+    }
+    ENG_CUDA(cudaMemcpyAsync(E->d_step, step.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_pos, pos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_status, zero.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_tok, zero.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_prng, prng.data(), sizeof(uint64_t) * prng.size(), cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_pol, dp.data(), sizeof(DevPolicy) * n, cudaMemcpyHostToDevice, s));
+    if (st) st->h2d_bytes += n * (4 * sizeof(int) + 32 + sizeof(DevPolicy));
+    ENG_CUDA(cudaEventRecord(E->ev[0], s));
+    // prefill: all prompt tokens (of active requests) as columns, chunked; chunking is invisible in
+    // the bits because every column is independent (batch invariance)
+    std::vector<int> ctok, cpos, creq, lin, lout;
+    uint64_t nl = 0;
+    auto flush = [&]() -> int {
+        if (ctok.empty()) return DETGPU_OK;
+        const int nc = static_cast<int>(ctok.size());
+        ENG_CUDA(cudaMemcpyAsync(E->p_tok, ctok.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+        ENG_CUDA(cudaMemcpyAsync(E->p_pos, cpos.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+        ENG_CUDA(cudaMemcpyAsync(E->p_req, creq.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+        const int nlast = static_cast<int>(lin.size());
+        if (nlast > 0) {
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_in, lin.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_out, lout.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+        }
+        if (st) st->h2d_bytes += sizeof(int) * (3ull * nc + 2ull * nlast);
+        ENG_CUDA(forward(E, nc, E->p_tok, E->p_pos, E->p_req, false, nlast, &nl));
+        // the host vectors are reused next chunk: wait for the async copies to be consumed
+        ENG_CUDA(cudaStreamSynchronize(s));
+        ctok.clear();
+        cpos.clear();
+        creq.clear();
+        lin.clear();
+        lout.clear();
+        return DETGPU_OK;
+    };
+    for (uint32_t i = 0; i < n; ++i) {
+        if (pols[i].max_tokens == 0) continue;
+        for (uint32_t t = 0; t < lens[i]; ++t) {
+            if (static_cast<int>(ctok.size()) == E->col_cap)
+                if (int rc = flush()) return rc;
+            if (t + 1 == lens[i]) {
+                lin.push_back(static_cast<int>(ctok.size()));
+                lout.push_back(static_cast<int>(i));
+            }
+            ctok.push_back(static_cast<int>(prompts[i][t]));
+            cpos.push_back(static_cast<int>(t));
+            creq.push_back(static_cast<int>(i));
+        }
+    }
+    if (int rc = flush()) return rc;
+    ENG_CUDA(head_and_sample(E, E->tm_hlast, static_cast<int>(n), &nl));
+    ENG_CUDA(cudaEventRecord(E->ev[1], s));
+    // decode loop: one graph replay per step
+    cudaGraphExec_t gx = nullptr;
+    if (tmax > 1)
+        if (int rc = get_graph(E, static_cast<int>(n), &gx)) return rc;
+    for (int t = 1; t < tmax; ++t) ENG_CUDA(cudaGraphLaunch(gx, s));
+    ENG_CUDA(cudaEventRecord(E->ev[2], s));
+    ENG_CUDA(cudaEventSynchronize(E->ev[2]));
+    if (st) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, E->ev[0], E->ev[1]);
+        cudaEventElapsedTime(&b, E->ev[1], E->ev[2]);
+        st->prefill_ms += a;
+        st->decode_ms += b;
+        st->decode_steps += static_cast<uint64_t>(tmax - 1);
+        st->kernel_launches += nl + static_cast<uint64_t>(tmax - 1) * E->launches_per_step;
+    }
+    return DETGPU_OK;
+}
+
+int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* const* tokens_out,
+                  float* const* logits_out, uint8_t* out_hash, detgpu_stats* st) {
+    const int V = E->cfg.V;
+    cudaStream_t s = E->stream;
+    std::vector<int> status(n);
+    ENG_CUDA(cudaMemcpy(status.data(), E->d_status, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < n; ++i) {
+        if (status[i] == DETGPU_ENONFINITE) return fail(E, DETGPU_EINVAL, "det_softmax: non-finite value");
+        if (status[i] != 0) return fail(E, DETGPU_EINVAL, "decode: zero probability mass after truncation");
+    }
+    Timer tcopy;
+    std::vector<uint32_t> toks(size_t(n) * std::max(E->tcap, 1));
+    if (E->tcap > 0)
+        ENG_CUDA(cudaMemcpy(toks.data(), E->tok_hist, sizeof(uint32_t) * size_t(n) * E->tcap, cudaMemcpyDeviceToHost));
+    if (st) st->d2h_bytes += sizeof(uint32_t) * size_t(n) * E->tcap;
+    for (uint32_t i = 0; i < n; ++i)
+        if (tokens_out && tokens_out[i] && pols[i].max_tokens)
+            std::memcpy(tokens_out[i], &toks[size_t(i) * E->tcap], sizeof(uint32_t) * pols[i].max_tokens);
+    double copy_ms = tcopy.ms(), hash_ms = 0;
+    // logits: D2H through two pinned staging buffers, hashing / copying piece k while k+1 lands
+    const size_t piece = E->pinned_floats;
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t T = pols[i].max_tokens;
+        const bool want_logits = logits_out && logits_out[i];
+        const bool want_hash = out_hash != nullptr;
+        if (!want_logits && !want_hash) continue;
+        Sha256 sha;
+        if (want_hash) {
+            sha.update(&T, 4);
+            if (T) sha.update(&toks[size_t(i) * E->tcap], 4 * size_t(T));
+            sha.update(&T, 4);
+        }
+        const size_t total = size_t(T) * V;
+        const float* src = E->trace + size_t(i) * E->slot_stride;
+        size_t done = 0;
+        int buf = 0;
+        size_t inflight = std::min(piece, total);
+        if (total > 0) ENG_CUDA(cudaMemcpyAsync(E->pinned[0], src, sizeof(float) * inflight, cudaMemcpyDeviceToHost, s));
+        while (done < total) {
+            Timer tw;
+            ENG_CUDA(cudaStreamSynchronize(s));
+            copy_ms += tw.ms();
+            const size_t cur = inflight;
+            const size_t next_off = done + cur;
+            size_t next = 0;
+            if (next_off < total) {
+                next = std::min(piece, total - next_off);
+                ENG_CUDA(cudaMemcpyAsync(E->pinned[buf ^ 1], src + next_off, sizeof(float) * next,
+                                         cudaMemcpyDeviceToHost, s));
+            }
+            Timer th;
+            const float* hp = E->pinned[buf];
+            if (want_logits) std::memcpy(logits_out[i] + done, hp, sizeof(float) * cur);
+            if (want_hash) {
+                // step boundaries inside this piece: each step is prefixed by its u32 vocab size
+                size_t off = 0;
+                while (off < cur) {
+                    const size_t g = done + off;
+                    if (g % V == 0) sha.update(&V, 4);
+                    const size_t run = std::min(cur - off, size_t(V) - g % V);
+                    sha.update(hp + off, 4 * run);
+                    off += run;
+                }
+            }
+            hash_ms += th.ms();
+            done += cur;
+            inflight = next;
+            buf ^= 1;
+        }
+        if (st) st->d2h_bytes += 4 * total;
+        if (want_hash) sha.final(out_hash + 32 * size_t(i));
+    }
+    if (st) {
+        st->d2h_ms += static_cast<float>(copy_ms);
+        st->hash_ms += static_cast<float>(hash_ms);
+    }
+    return DETGPU_OK;
+}
+
+}  // namespace
+
+}  // namespace detgpu
+
+using namespace detgpu;
+
+struct detgpu_engine {
+    std::unique_ptr<Engine> e;
+};
+
+extern "C" {
+
+int detgpu_arch_supported(const char* arch) {
+    return arch && (std::strcmp(arch, "archA") == 0 || std::strcmp(arch, "archB") == 0 || std::strcmp(arch, "b200") == 0);
+}
+
+int detgpu_create(int device, const char* model_id, const char* arch, uint32_t max_batch, uint32_t max_context,
+                  detgpu_engine** out) {
+    if (out == nullptr || model_id == nullptr || arch == nullptr) return fail(nullptr, DETGPU_EINVAL, "null argument");
+    *out = nullptr;
+    if (!detgpu_arch_supported(arch))
+        return fail(nullptr, DETGPU_EINVAL, std::string("infer: unknown arch profile '") + arch + "'");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(nullptr, DETGPU_ENODEV, "no such CUDA device");
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major != 10) return fail(nullptr, DETGPU_ENODEV, "detgpu needs an sm_100 (B200) device");
+    auto E = std::make_unique<Engine>();
+    E->device = device;
+    E->model_id = model_id;
+    E->arch = arch;
+    E->max_batch = std::max<uint32_t>(1, std::min<uint32_t>(max_batch, 256));
+    E->max_context = std::max<uint32_t>(1, max_context);
+    cudaSetDevice(device);
+    Engine* Ep = E.get();
+    {
+        Engine* E = Ep;   // for ENG_CUDA
+        ENG_CUDA(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
+        for (auto& ev : E->ev) ENG_CUDA(cudaEventCreate(&ev));
+        if (std::strcmp(arch, "b200") != 0) {
+            E->toy = true;
+            if (int rc = toy_init(E->toyw, model_id, std::strcmp(arch, "archA") == 0 ? 0 : 1, E->stream))
+                return fail(E, rc, "toy model init failed");
+        } else {
+            const ModelConfig* c = find_model_config(model_id);
+            if (c == nullptr)
+                return fail(nullptr, DETGPU_EINVAL,
+                            std::string("unknown model config for '") + model_id + "' (expected llama-tiny[:tag] or llama3-8b[:tag])");
+            E->cfg = *c;
+            if (int rc = init_weights(E)) return rc;
+            if (int rc = init_buffers(E)) return rc;
+            E->pinned_floats = size_t(1) << 24;   // 64 MiB per staging buffer
+            for (auto& p : E->pinned) ENG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(float) * E->pinned_floats));
+        }
+        ENG_CUDA(cudaStreamSynchronize(E->stream));
+    }
+    *out = new detgpu_engine{std::move(E)};
+    return DETGPU_OK;
+}
+
+void detgpu_destroy(detgpu_engine* h) { delete h; }
+
+const char* detgpu_last_error(const detgpu_engine* h) { return h ? h->e->err.c_str() : detgpu_global_error(); }
+
+int detgpu_get_model_info(const detgpu_engine* h, detgpu_model_info* o) {
+    if (!h || !o) return DETGPU_EINVAL;
+    const Engine* E = h->e.get();
+    std::memset(o, 0, sizeof(*o));
+    if (E->toy) {
+        o->toy = 1;
+        o->vocab = kToyVocab;
+        o->d_model = kToyDim;
+        o->n_layers = 2;
+        o->n_params = 2 * kToyVocab * kToyDim + 2 * kToyDim * kToyDim;
+        o->weight_bytes = 4 * o->n_params;
+        return DETGPU_OK;
+    }
+    o->n_layers = E->cfg.L;
+    o->d_model = E->cfg.d;
+    o->n_heads = E->cfg.hq;
+    o->n_kv_heads = E->cfg.hkv;
+    o->head_dim = E->cfg.hd;
+    o->ffn = E->cfg.F;
+    o->vocab = E->cfg.V;
+    o->rope_theta = static_cast<float>(E->cfg.theta);
+    o->rms_eps = E->cfg.eps;
+    o->n_params = E->n_params;
+    o->weight_bytes = 2 * E->n_params;
+    return DETGPU_OK;
+}
+
+int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* prompts, const uint32_t* prompt_lens,
+                    const detgpu_policy* policies, const uint64_t* seeds, uint32_t batch_size,
+                    uint32_t* const* tokens_out, float* const* logits_out, uint8_t* out_hash, uint32_t flags,
+                    detgpu_stats* stats) {
+    if (h == nullptr) return fail(nullptr, DETGPU_EINVAL, "null engine");
+    Engine* E = h->e.get();
+    cudaSetDevice(E->device);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (batch_size == 0) return fail(E, DETGPU_EINVAL, "infer_batch: batch_size must be positive");
+    if (n_req == 0) return DETGPU_OK;
+    if (!prompts || !prompt_lens || !policies || !seeds) return fail(E, DETGPU_EINVAL, "null argument");
+    const uint32_t vocab = E->toy ? kToyVocab : static_cast<uint32_t>(E->cfg.V);
+    // start_run validation (detcore.cpp:332-343), all requests before any work
+    for (uint32_t i = 0; i < n_req; ++i) {
+        const std::string perr = validate_policy(policies[i]);
+        if (!perr.empty()) return fail(E, DETGPU_EINVAL, "infer: " + perr);
+        for (uint32_t t = 0; t < prompt_lens[i]; ++t)
+            if (prompts[i][t] >= vocab) return fail(E, DETGPU_EINVAL, "infer: prompt token out of vocabulary");
+        if (!E->toy) {
+            if (prompt_lens[i] == 0 && policies[i].max_tokens > 0)
+                return fail(E, DETGPU_EINVAL, "infer: empty prompt (a transformer needs a position to predict from)");
+            if (uint64_t(prompt_lens[i]) + policies[i].max_tokens > E->max_context)
+                return fail(E, DETGPU_EINVAL, "infer: prompt + max_tokens exceeds the engine's max_context");
+        }
+    }
+    if (E->toy)
+        return toy_generate(E->toyw, n_req, prompts, prompt_lens, policies, seeds, batch_size, tokens_out, logits_out,
+                            out_hash, flags, stats, E->stream, &E->err);
+    const uint32_t group = std::min(batch_size, E->max_batch);
+    Timer total;
+    for (uint32_t base = 0; base < n_req; base += group) {
+        const uint32_t n = std::min(group, n_req - base);
+        if (stats) stats->h2d_bytes += 0;
+        if (int rc = run_group(E, n, prompts + base, prompt_lens + base, policies + base, seeds + base, stats)) return rc;
+        if (stats)
+            for (uint32_t i = 0; i < n; ++i) stats->tokens += policies[base + i].max_tokens;
+        if (!(flags & DETGPU_F_DEVICE_ONLY)) {
+            uint32_t* const* to = tokens_out ? tokens_out + base : nullptr;
+            float* const* lo = logits_out ? logits_out + base : nullptr;
+            if (int rc = collect_group(E, n, policies + base, to, lo, out_hash ? out_hash + 32 * size_t(base) : nullptr, stats))
+                return rc;
+        } else {
+            std::vector<int> status(n);
+            ENG_CUDA(cudaMemcpy(status.data(), E->d_status, sizeof(int) * n, cudaMemcpyDeviceToHost));
+            for (uint32_t i = 0; i < n; ++i)
+                if (status[i] != 0) return fail(E, DETGPU_EINVAL, "decode: non-finite value or zero probability mass");
+        }
+    }
+    // max_tokens == 0 requests: tokens empty, canonical bytes = [0][0]
+    if (out_hash && !(flags & DETGPU_F_DEVICE_ONLY))
+        for (uint32_t i = 0; i < n_req; ++i)
+            if (policies[i].max_tokens == 0) hash_canonical(nullptr, 0, nullptr, vocab, out_hash + 32 * size_t(i));
+    (void)total;
+    return DETGPU_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+void* detgpu_stream(const detgpu_engine* h) { return h ? static_cast<void*>(h->e->stream) : nullptr; }
+
+// One decode forward + lm_head + sample for `ncols` slots at context `ctx`, launched without graph
+// or PDL, with a CUDA event after every launch on the engine stream. ms_by_class[k] is the mean
+// time per step spent in kernel class k (0 norm, 1 qkv gemm, 2 attention, 3 o gemm, 4 gate/up gemm,
+// 5 down gemm, 6 lm_head gemm, 7 sample); launches_by_class[k] the launches per step.
+int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t reps, float* ms_by_class,
+                               uint32_t* launches_by_class) {
+    if (h == nullptr || h->e->toy) return fail(nullptr, DETGPU_EINVAL, "profile: transformer engine required");
+    Engine* E = h->e.get();
+    cudaSetDevice(E->device);
+    if (ncols == 0 || ncols > E->max_batch || ctx == 0 || ctx > E->max_context || reps == 0)
+        return fail(E, DETGPU_EINVAL, "profile: bad ncols/ctx/reps");
+    if (int rc = ensure_outputs(E, static_cast<int>(ncols), 2)) return rc;
+    std::vector<int> step(ncols, 0), pos(ncols, static_cast<int>(ctx) - 1), tok(ncols, 1), zero(ncols, 0);
+    std::vector<uint64_t> prng(size_t(ncols) * 4);
+    std::vector<DevPolicy> dp(ncols);
+    for (uint32_t i = 0; i < ncols; ++i) {
+        prng_seeded(i, &prng[size_t(i) * 4]);
+        dp[i] = DevPolicy{DETGPU_GREEDY, 0, 0.0f, 2};
+    }
+    ENG_CUDA(cudaMemcpy(E->d_prng, prng.data(), sizeof(uint64_t) * prng.size(), cudaMemcpyHostToDevice));
+    ENG_CUDA(cudaMemcpy(E->d_pol, dp.data(), sizeof(DevPolicy) * ncols, cudaMemcpyHostToDevice));
+    std::vector<std::pair<cudaEvent_t, int>> trail;
+    const bool pdl = E->use_pdl;
+    E->use_pdl = false;
+    std::vector<double> acc(kProfN, 0.0);
+    std::vector<uint32_t> cnt(kProfN, 0);
+    cudaError_t err = cudaSuccess;
+    for (uint32_t r = 0; r < reps && err == cudaSuccess; ++r) {
+        cudaMemcpyAsync(E->d_step, step.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, E->stream);
+        cudaMemcpyAsync(E->d_pos, pos.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, E->stream);
+        cudaMemcpyAsync(E->d_tok, tok.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, E->stream);
+        cudaMemcpyAsync(E->d_status, zero.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, E->stream);
+        trail.clear();
+        E->prof = &trail;
+        mark(E, -1);
+        err = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
+        if (err == cudaSuccess) err = head_and_sample(E, E->tm_h, static_cast<int>(ncols), nullptr);
+        E->prof = nullptr;
+        if (err == cudaSuccess) err = cudaStreamSynchronize(E->stream);
+        for (size_t i = 1; i < trail.size() && err == cudaSuccess; ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, trail[i - 1].first, trail[i].first);
+            acc[trail[i].second] += ms;
+            if (r == 0) cnt[trail[i].second] += 1;
+        }
+        for (auto& t : trail) cudaEventDestroy(t.first);
+    }
+    E->use_pdl = pdl;
+    ENG_CUDA(err);
+    for (int k = 0; k < kProfN; ++k) {
+        if (ms_by_class) ms_by_class[k] = static_cast<float>(acc[k] / reps);
+        if (launches_by_class) launches_by_class[k] = cnt[k];
+    }
+    return DETGPU_OK;
+}
+
+}  // extern "C"

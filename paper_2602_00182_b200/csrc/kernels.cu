@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       const int* __restrict__ col_token,
                                                       const __nv_bfloat16* __restrict__ gamma,
                                                       __nv_bfloat16* __restrict__ out, const int* __restrict__ col_index,
-                                                      int d, float eps) {
+                                                      const int* __restrict__ out_index, int d, float eps) {
     __shared__ float scratch[32];
     pdl_trigger();
     pdl_wait();
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
     s = block_tree_combine<8>(s, scratch);
     const float ms = __fdiv_rn(s, static_cast<float>(d));
     const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
-    __nv_bfloat16* o = out + static_cast<int64_t>(col) * d + base;
+    const int orow = out_index != nullptr ? out_index[col] : col;
+    __nv_bfloat16* o = out + static_cast<int64_t>(orow) * d + base;
 #pragma unroll
     for (int j = 0; j < E; ++j) o[j] = f2bf(__fmul_rn(__fmul_rn(v[j], rstd), bf2f(gamma[base + j])));
 }
@@ -553,22 +554,35 @@ cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStream_t str
 cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
                            const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* col_index, int ncols, int d,
                            float eps, cudaStream_t stream, bool pdl) {
+    return launch_rmsnorm_ex(x_in, x_out, embed, col_token, gamma, out, col_index, nullptr, ncols, d, eps, stream, pdl);
+}
+
+cudaError_t launch_rmsnorm_ex(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
+                              const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index, const int* out_index,
+                              int ncols, int d, float eps, cudaStream_t stream, bool pdl) {
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = make_cfg(dim3(ncols), dim3(256), 0, stream, attr, pdl);
+    const int* ii = in_index;
+    const int* oi = out_index;
     switch (d) {
         case 256:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<1>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<1>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
         case 512:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<2>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<2>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
         case 1024:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<4>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<4>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
         case 2048:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<8>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<8>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
         case 4096:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<16>, x_in, x_out, embed, col_token, gamma, out, col_index, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<16>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
         default:
             return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_rmsnorm_gather(const float* x, const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index,
+                                  const int* out_index, int n, int d, float eps, cudaStream_t stream, bool pdl) {
+    return launch_rmsnorm_ex(x, nullptr, nullptr, nullptr, gamma, out, in_index, out_index, n, d, eps, stream, pdl);
 }
 
 cudaError_t launch_expf(const float* x, float* y, int64_t n, cudaStream_t stream) {

@@ -19,6 +19,12 @@ cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16*
                            const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* col_index, int ncols, int d,
                            float eps, cudaStream_t stream, bool pdl);
 
+cudaError_t launch_rmsnorm_ex(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
+                              const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index, const int* out_index,
+                              int ncols, int d, float eps, cudaStream_t stream, bool pdl);
+// out[out_index[i]] = rmsnorm(x[in_index[i]]) for i < n
+cudaError_t launch_rmsnorm_gather(const float* x, const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index,
+                                  const int* out_index, int n, int d, float eps, cudaStream_t stream, bool pdl);
 cudaError_t launch_expf(const float* x, float* y, int64_t n, cudaStream_t stream);
 cudaError_t launch_tree_sum(const float* x, float* out, int rows, int n, cudaStream_t stream);
 cudaError_t launch_init_tensor(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp,

@@ -42,6 +42,25 @@ def test_gemm_matches_fp64(n_out, K, ncols):
     assert (err <= bound).all(), f"max err {err.max().item()} bound {bound.min().item()}"
 
 
+@pytest.mark.parametrize("n_out,K,ncols,scale", [(128, 64, 3, 1.0), (256, 4096, 17, 0.02), (128, 14336, 5, 0.01),
+                                                  (384, 256, 70, 30.0)])
+def test_gemm_bit_exact_with_b200_profile(n_out, K, ncols, scale):
+    """Every output equals the oracle's b200 accumulation profile bit for bit."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+
+    g = torch.Generator().manual_seed(K + ncols)
+    W = _rand_bf16((n_out, K), g, scale)
+    X = _rand_bf16((ncols, K), g)
+    Y = _gemm(W, X)
+    Wn = W.view(torch.int16).cpu().numpy().view(np.uint16)
+    Xn = X.view(torch.int16).cpu().numpy().view(np.uint16)
+    ref = O.gemm(Wn, Xn)
+    assert (Y.cpu().numpy().view(np.uint32) == ref.view(np.uint32)).all()
+
+
 def test_batch_invariance_bitwise():
     import torch
 
