@@ -658,12 +658,34 @@ static float tc_dot(const uint16_t* w, const uint16_t* x, int K) {
     return c;
 }
 
+// The b200 GEMM splits K into S fixed segments (a function of the shape only; engine gemm.cu
+// gemm_ksplit): S = min(8, K/64, max(1, 148 / (rows/128))), segment s = 64-wide k-blocks
+// [s*nkb/S, (s+1)*nkb/S). Each segment is one tc_dot chain; the S partials are combined with the
+// reference tree in segment order.
+static int ksplit(int rows, int cols) {
+    const int tiles = rows / 128, nkb = cols / 64;
+    int s = 148 / (tiles > 0 ? tiles : 1);
+    s = std::max(1, std::min(8, s));
+    return std::min(s, std::max(nkb, 1));
+}
+static float tc_dot_segmented(const uint16_t* w, const uint16_t* x, int K, int S) {
+    if (S <= 1) return tc_dot(w, x, K);
+    const int nkb = K / 64;
+    float part[8];
+    for (int s = 0; s < S; ++s) {
+        const int k0 = (s * nkb / S) * 64, k1 = ((s + 1) * nkb / S) * 64;
+        part[s] = tc_dot(w + k0, x + k0, k1 - k0);
+    }
+    return tree_reduce(part, size_t(S));
+}
+
 static int g_gemm_mode = 0;   // 0: b200 (tcgen05) profile ; 1: reference canonical tree
 // y[r] = W[r,:] . x under the active accumulation profile. Profile 1 is det_matvec canonical_tree
 // (detcore.cpp:180-181): products of two bf16 values are exact in f32, then the reference tree.
 static void gemv(const uint16_t* W, int rows, int cols, const uint16_t* x, float* y) {
     if (g_gemm_mode == 0) {
-        parallel_for(rows, [&](int64_t r) { y[r] = tc_dot(W + size_t(r) * cols, x, cols); });
+        const int S = ksplit(rows, cols);
+        parallel_for(rows, [&](int64_t r) { y[r] = tc_dot_segmented(W + size_t(r) * cols, x, cols, S); });
         return;
     }
     parallel_for(rows, [&](int64_t r) {

@@ -34,7 +34,7 @@ const char* detgpu_global_error(void) { return detgpu::global_error().c_str(); }
 
 int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy, void* stream) {
     CUtensorMap tw, tx;
-    if (!make_tmap_bf16(&tw, W, K, n_out, 128) || !make_tmap_bf16(&tx, X, K, ncols, 64)) {
+    if (!make_tmap_weights(&tw, W, n_out, K, false) || !make_tmap_bf16(&tx, X, K, ncols, 64)) {
         set_global_error("cuTensorMapEncodeTiled failed");
         return DETGPU_ECUDA;
     }
@@ -96,8 +96,13 @@ int detgpu_k_attention(const void* q, const void* kcache, const void* vcache, co
     const size_t ws_bytes = attn_workspace_bytes(a);
     DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, static_cast<cudaStream_t>(stream)));
     a.ws = ws;
+    int* tickets = nullptr;
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tickets), sizeof(int) * ncols * hkv, static_cast<cudaStream_t>(stream)));
+    DETGPU_CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(int) * ncols * hkv, static_cast<cudaStream_t>(stream)));
+    a.tickets = tickets;
     cudaError_t e = launch_attention(a, static_cast<cudaStream_t>(stream), false);
     cudaFreeAsync(ws, static_cast<cudaStream_t>(stream));
+    cudaFreeAsync(tickets, static_cast<cudaStream_t>(stream));
     DETGPU_CUDA_TRY(e);
     return DETGPU_OK;
 }

@@ -1,0 +1,266 @@
+// Paged decode attention with a fixed KV-chunk order.
+//
+// One CTA per (chunk, kv head, query column); the G = hq/hkv query heads of a kv head share the
+// chunk's K/V in shared memory. Per query head:
+//   s_p = tree_d(q_d * k_pd) * (1/sqrt(hd))      products of bf16 pairs are exact in f32
+//   m = max_p s_p ; e_p = exp(s_p - m) ; l = tree_p(e_p) ; o_d = fma chain over p in order
+// and the chunks are combined in chunk order by whichever CTA of the (column, kv head) finishes
+// last (a ticket elects the combiner; the combination itself is order-fixed):
+//   a_c = exp(m_c - max m) ; out_d = bf16( (sum_c fma o_cd a_c) / (sum_c fma l_c a_c) )
+// Chunk boundaries are positions 128c, so split-KV parallelism never changes a bit and prefill
+// queries see exactly the same arithmetic as decode steps.
+#include <cfloat>
+
+#include "detmath.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace detgpu {
+
+namespace {
+
+constexpr int kNT = 256;           // threads per CTA
+constexpr int kNW = kNT / 32;
+
+template <int HD, int G>
+__global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, float scale) {
+    constexpr int CH = kAttnChunk;
+    constexpr int E = HD / 32;                       // q/k elements per lane in a dot product
+    constexpr int CHAINS = G * HD;                   // (head, d) accumulators of the PV product
+    constexpr int CPT = (CHAINS + kNT - 1) / kNT;    // chains per thread
+    extern __shared__ __align__(16) uint8_t attn_dsm[];
+    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_dsm);
+    __nv_bfloat16* sV = sK + CH * HD;
+    __shared__ float sQ[G * HD];
+    __shared__ float sS[G * CH];
+    __shared__ float sM[G], sL[G];
+    __shared__ int s_last;
+
+    pdl_trigger();
+    const int c = blockIdx.x, kvh = blockIdx.y, col = blockIdx.z;
+    pdl_wait();
+    const int pos = a.col_pos[col];
+    if (pos < 0) return;
+    const int ctx = pos + 1;
+    const int p0 = c * CH;
+    if (p0 >= ctx) return;
+    const int n = min(CH, ctx - p0);
+    const int slot = a.col_req[col];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // K/V rows: page ids of the chunk first, then every 16-byte vector with cp.async
+    constexpr int VPR = HD * 2 / 16;
+    {
+        const int* bt = a.block_table + static_cast<int64_t>(slot) * a.max_pages + p0 / a.page;
+        for (int i = tid; i < n * VPR; i += kNT) {
+            const int r = i / VPR, v = i % VPR;
+            const int p = p0 + r;
+            const int pid = __ldg(bt + r / a.page);
+            const int64_t off = ((static_cast<int64_t>(pid) * a.hkv + kvh) * a.page + p % a.page) * HD;
+            cp_async_16(sK + r * HD + v * 8, a.kcache + off + v * 8);
+            cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
+        }
+        cp_async_commit();
+    }
+    const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    for (int i = tid; i < G * HD; i += kNT) sQ[i] = bf2f(qsrc[i]);
+    cp_async_wait_all();
+    __syncthreads();
+
+    // scores: each warp takes two positions per step; 2G butterflies interleaved
+    float q[G][E];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < E; ++j) q[g][j] = sQ[g * HD + lane * E + j];
+    for (int p = warp * 2; p < n; p += 2 * kNW) {
+        const bool two = p + 1 < n;
+        float k0[E], k1[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            k0[j] = bf2f(sK[p * HD + lane * E + j]);
+            k1[j] = two ? bf2f(sK[(p + 1) * HD + lane * E + j]) : 0.0f;
+        }
+        float s0[G], s1[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float a0[E], a1[E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                a0[j] = __fmul_rn(q[g][j], k0[j]);
+                a1[j] = __fmul_rn(q[g][j], k1[j]);
+            }
+            s0[g] = local_tree_sum<E>(a0);
+            s1[g] = local_tree_sum<E>(a1);
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                s0[g] = __fadd_rn(s0[g], __shfl_xor_sync(0xffffffffu, s0[g], off));
+                s1[g] = __fadd_rn(s1[g], __shfl_xor_sync(0xffffffffu, s1[g], off));
+            }
+        }
+        if (lane < G) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g == lane) {
+                    sS[g * CH + p] = __fmul_rn(s0[g], scale);
+                    if (two) sS[g * CH + p + 1] = __fmul_rn(s1[g], scale);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // chunk softmax pieces: warp g owns head g (4 positions per lane)
+    for (int g = warp; g < G; g += kNW) {
+        float sv[4], e[4];
+        float m = -FLT_MAX;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = lane * 4 + j;
+            sv[j] = p < n ? sS[g * CH + p] : 0.0f;
+            if (p < n) m = fmaxf(m, sv[j]);
+        }
+        m = warp_max(m);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = lane * 4 + j;
+            e[j] = p < n ? det_expf(__fsub_rn(sv[j], m)) : kNegZero;
+            sS[g * CH + p] = e[j];
+        }
+        float l = local_tree_sum<4>(e);
+        l = warp_tree_sum(l);
+        if (lane == 0) {
+            sM[g] = m;
+            sL[g] = l;
+        }
+    }
+    __syncthreads();
+
+    // o: chain (g, d) = fma over positions in order
+    float acc[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
+    if (tid < CHAINS) {
+        const int d = tid % HD;   // every chain of this thread has the same d (kNT % HD == 0)
+#pragma unroll 4
+        for (int p = 0; p < n; ++p) {
+            const float v = bf2f(sV[p * HD + d]);
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const int ch = tid + j * kNT;
+                if (ch < CHAINS) acc[j] = __fmaf_rn(sS[(ch / HD) * CH + p], v, acc[j]);
+            }
+        }
+    }
+    const int nch = (ctx + CH - 1) / CH;
+    __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    if (nch == 1) {
+        // single chunk: the combine weight is exp(0) == 1 exactly
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int ch = tid + j * kNT;
+            if (ch < CHAINS)
+                outp[ch] = f2bf(__fdiv_rn(__fmaf_rn(acc[j], 1.0f, 0.0f), __fmaf_rn(sL[ch / HD], 1.0f, 0.0f)));
+        }
+        return;
+    }
+    float* wsb = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2);
+    float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 2);
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        const int ch = tid + j * kNT;
+        if (ch < CHAINS) ws[(ch / HD) * (HD + 2) + 2 + ch % HD] = acc[j];
+    }
+    if (tid < G) {
+        ws[tid * (HD + 2)] = sM[tid];
+        ws[tid * (HD + 2) + 1] = sL[tid];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        int* t = a.tickets + static_cast<int64_t>(col) * a.hkv + kvh;
+        const int prev = atomicAdd(t, 1);
+        s_last = prev == nch - 1;
+        if (s_last) *t = 0;   // re-armed for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        const int ch = tid + j * kNT;
+        if (ch >= CHAINS) continue;
+        const int g = ch / HD, d = ch % HD;
+        const float* base = wsb + g * (HD + 2);
+        float M = -FLT_MAX;
+        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(base + cc * cstride));
+        float L = 0.0f, O = 0.0f;
+        for (int cc = 0; cc < nch; ++cc) {
+            const float* w = base + cc * cstride;
+            const float al = det_expf(__fsub_rn(__ldcg(w), M));
+            L = __fmaf_rn(__ldcg(w + 1), al, L);
+            O = __fmaf_rn(__ldcg(w + 2 + d), al, O);
+        }
+        outp[ch] = f2bf(__fdiv_rn(O, L));
+    }
+}
+
+template <int HD, int G>
+cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(dsm));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.max_chunks, a.hkv, a.ncols);
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = dsm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(HD)));
+    return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G>, a, scale);
+}
+
+}  // namespace
+
+size_t attn_workspace_bytes(const AttnParams& a) {
+    const int G = a.hq / a.hkv;
+    return sizeof(float) * static_cast<size_t>(a.ncols) * a.hkv * a.max_chunks * G * (a.hd + 2);
+}
+
+cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    if (a.hkv <= 0 || a.hq % a.hkv != 0 || a.page < 16 || a.page % 16 != 0) return cudaErrorInvalidValue;
+    const int G = a.hq / a.hkv;
+    if (a.hd == 128) {
+        switch (G) {
+            case 1: return launch_hg<128, 1>(a, stream, pdl);
+            case 2: return launch_hg<128, 2>(a, stream, pdl);
+            case 4: return launch_hg<128, 4>(a, stream, pdl);
+            case 8: return launch_hg<128, 8>(a, stream, pdl);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    if (a.hd == 64) {
+        switch (G) {
+            case 1: return launch_hg<64, 1>(a, stream, pdl);
+            case 2: return launch_hg<64, 2>(a, stream, pdl);
+            case 4: return launch_hg<64, 4>(a, stream, pdl);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace detgpu

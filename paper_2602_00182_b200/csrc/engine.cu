@@ -68,6 +68,7 @@ struct Engine {
     int pages_per_slot = 0, total_pages = 0, max_chunks = 0;
     int* block_table = nullptr;
     float* attn_ws = nullptr;
+    int* attn_tickets = nullptr;
     float *rope_cos = nullptr, *rope_sin = nullptr;
     // prefill plan
     int *p_tok = nullptr, *p_pos = nullptr, *p_req = nullptr, *p_last_in = nullptr, *p_last_out = nullptr;
@@ -143,9 +144,9 @@ int init_weights(Engine* E) {
     ENG_CUDA(E->alloc(&E->lm_head, size_t(V) * d));
     ENG_CUDA(E->alloc(&E->final_norm, d));
     ENG_CUDA(launch_init_tensor(E->embed, seed(0), V, d, 0, 0, 1, 0, s));
-    ENG_CUDA(launch_init_tensor(E->lm_head, seed(1), V, d, 4 + sd, 0, 1, 0, s));
+    ENG_CUDA(launch_init_tensor(E->lm_head, seed(1), V, d, 4 + sd, 0, 1, 0, s, true));
     ENG_CUDA(launch_init_tensor(E->final_norm, seed(2), 1, d, 0, 1, 1, 0, s));
-    if (!make_tmap_bf16(&E->tm_lm, E->lm_head, d, V, 128)) return fail(E, DETGPU_ECUDA, "tensor map (lm_head)");
+    if (!make_tmap_weights(&E->tm_lm, E->lm_head, V, d, true)) return fail(E, DETGPU_ECUDA, "tensor map (lm_head)");
     E->n_params = 2ull * V * d + d;
     E->layers.resize(c.L);
     for (int l = 0; l < c.L; ++l) {
@@ -159,16 +160,16 @@ int init_weights(Engine* E) {
         ENG_CUDA(launch_init_tensor(Ly.attn_norm, seed(layer_tensor_id(l, kAttnNorm)), 1, d, 0, 1, 1, 0, s));
         ENG_CUDA(launch_init_tensor(Ly.ffn_norm, seed(layer_tensor_id(l, kFfnNorm)), 1, d, 0, 1, 1, 0, s));
         // fused QKV rows: [wq ; wk ; wv]
-        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWq)), qd, d, sd, 0, 1, 0, s));
-        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWk)), kd, d, sd, 0, 1, qd, s));
-        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWv)), kd, d, sd, 0, 1, qd + kd, s));
-        ENG_CUDA(launch_init_tensor(Ly.wo, seed(layer_tensor_id(l, kWo)), d, qd, sq, 0, 1, 0, s));
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWq)), qd, d, sd, 0, 1, 0, s, true));
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWk)), kd, d, sd, 0, 1, qd, s, true));
+        ENG_CUDA(launch_init_tensor(Ly.wqkv, seed(layer_tensor_id(l, kWv)), kd, d, sd, 0, 1, qd + kd, s, true));
+        ENG_CUDA(launch_init_tensor(Ly.wo, seed(layer_tensor_id(l, kWo)), d, qd, sq, 0, 1, 0, s, true));
         // gate/up interleaved by row: physical 2j = gate j, 2j+1 = up j (SwiGLU epilogue pairs)
-        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWgate)), F, d, sd, 0, 2, 0, s));
-        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWup)), F, d, sd, 0, 2, 1, s));
-        ENG_CUDA(launch_init_tensor(Ly.wdown, seed(layer_tensor_id(l, kWdown)), d, F, sf, 0, 1, 0, s));
-        if (!make_tmap_bf16(&Ly.tm_qkv, Ly.wqkv, d, qd + 2 * kd, 128) || !make_tmap_bf16(&Ly.tm_o, Ly.wo, qd, d, 128) ||
-            !make_tmap_bf16(&Ly.tm_gu, Ly.wgu, d, 2 * F, 128) || !make_tmap_bf16(&Ly.tm_down, Ly.wdown, F, d, 128))
+        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWgate)), F, d, sd, 0, 2, 0, s, true));
+        ENG_CUDA(launch_init_tensor(Ly.wgu, seed(layer_tensor_id(l, kWup)), F, d, sd, 0, 2, 1, s, true));
+        ENG_CUDA(launch_init_tensor(Ly.wdown, seed(layer_tensor_id(l, kWdown)), d, F, sf, 0, 1, 0, s, true));
+        if (!make_tmap_weights(&Ly.tm_qkv, Ly.wqkv, qd + 2 * kd, d, true) || !make_tmap_weights(&Ly.tm_o, Ly.wo, d, qd, true) ||
+            !make_tmap_weights(&Ly.tm_gu, Ly.wgu, 2 * F, d, true) || !make_tmap_weights(&Ly.tm_down, Ly.wdown, d, F, true))
             return fail(E, DETGPU_ECUDA, "tensor map (layer)");
         E->n_params += 2ull * d + size_t(qd + 2 * kd) * d + size_t(d) * qd + 3ull * F * d;
     }
@@ -213,6 +214,8 @@ int init_buffers(Engine* E) {
         a.hd = c.hd;
         a.max_chunks = E->max_chunks;
         ENG_CUDA(E->alloc(&E->attn_ws, attn_workspace_bytes(a) / sizeof(float)));
+        ENG_CUDA(E->alloc(&E->attn_tickets, size_t(C) * c.hkv));
+        ENG_CUDA(cudaMemset(E->attn_tickets, 0, sizeof(int) * size_t(C) * c.hkv));
     }
     // RoPE tables, host binary64 -> f32; identical expression in the oracle.
     const int npos = static_cast<int>(E->max_context), h2 = c.hd / 2;
@@ -260,6 +263,7 @@ void mark(Engine* E, int cls) {
 }
 GemmParams gemm_base(int n_out, int k, int ncols) {
     GemmParams p{};
+    p.w_tiled = 1;   // engine weights are stored pre-tiled
     p.n_out = n_out;
     p.k = k;
     p.ncols = ncols;
@@ -310,6 +314,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.col_req = req;
         a.out = E->attn;
         a.ws = E->attn_ws;
+        a.tickets = E->attn_tickets;
         a.ncols = ncols;
         a.hq = c.hq;
         a.hkv = c.hkv;

@@ -89,6 +89,21 @@ __device__ __forceinline__ void epilogue_swiglu(const GemmParams& p, int row, in
     p.act[static_cast<int64_t>(col) * (p.n_out / 2) + (row >> 1)] = f2bf(__fmul_rn(sg, partner));
 }
 
+__device__ __forceinline__ void epilogue_any(const GemmParams& p, int row, int col, float v) {
+    if (p.mode == kEpiQkvRope || p.mode == kEpiSwiglu) {
+        const float partner = __shfl_xor_sync(0xffffffffu, v, 1);   // callers keep `col` warp-uniform
+        if (p.mode == kEpiQkvRope) epilogue_qkv(p, row, col, v, partner);
+        else epilogue_swiglu(p, row, col, v, partner);
+    } else {
+        epilogue_store(p, row, col, v);
+    }
+}
+
+// Grid (S, n_out/128, column groups), cluster (S,1,1): the S CTAs of a cluster own the same 128
+// weight rows and columns and the fixed K-segments [s*nkb/S, (s+1)*nkb/S) of the reduction. Each
+// runs its segment as one tcgen05 accumulation chain in TMEM; the S partial tiles are exchanged
+// through distributed shared memory and combined per element with the reference tree over the S
+// partials in segment order (detcore.cpp:135-150). S depends only on the GEMM shape.
 template <int NSUB>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -105,11 +120,15 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int col0 = blockIdx.y * (NSUB * SUB_N);
+    const int S = p.ksplit;
+    const int seg = blockIdx.x;                 // == %cluster_ctarank
+    const int m0 = blockIdx.y * BM;
+    const int col0 = blockIdx.z * (NSUB * SUB_N);
     const int ncols = min(NSUB * SUB_N, p.ncols - col0);
     const int nb = (ncols + SUB_N - 1) / SUB_N;
-    const int nkb = p.k / BK;
+    const int nkb_all = p.k / BK;
+    const int kb0 = seg * nkb_all / S, kb1 = (seg + 1) * nkb_all / S;
+    const int nkb = kb1 - kb0;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -129,36 +148,43 @@ __global__ void __launch_bounds__(256, 1)
     // Dependents only prefetch their own weights before griddepcontrol.wait, so they may launch now.
     pdl_trigger();
 
+    // Weight tile (128 rows x 64 k) through a 3D tensor map: pre-tiled weights are one contiguous
+    // 16 KB block per (tile, k-block) -> coordinate (0, 0, tile*nkb + kb); a plain row-major matrix
+    // is viewed as [rows][K/64][64] -> coordinate (0, kb, m0). Same smem image either way.
+    auto load_w = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int kb) {
+        if (p.w_tiled) tma_load_3d(dst, m, bar, 0, 0, blockIdx.y * nkb_all + kb, kEvictFirst);
+        else tma_load_3d(dst, m, bar, 0, kb, m0, kEvictFirst);
+    };
     if (warp == 0) {
         if (lane == 0) {
             const uint32_t stage_tx = A_BYTES + nb * B_BYTES;
             const int pre = min(STAGES, nkb);
             // Weight tiles do not depend on the previous kernel: stream them before the PDL wait.
-            for (int kb = 0; kb < pre; ++kb) {
-                mbar_arrive_expect_tx(&full[kb], stage_tx);
-                tma_load_2d(sA + kb * A_BYTES, &tmW, &full[kb], kb * BK, m0, kEvictFirst);
+            for (int i = 0; i < pre; ++i) {
+                mbar_arrive_expect_tx(&full[i], stage_tx);
+                load_w(sA + i * A_BYTES, &tmW, &full[i], kb0 + i);
             }
             pdl_wait();
-            for (int kb = 0; kb < pre; ++kb)
+            for (int i = 0; i < pre; ++i)
                 for (int j = 0; j < nb; ++j)
-                    tma_load_2d(sB + (kb * NSUB + j) * B_BYTES, &tmX, &full[kb], kb * BK, col0 + j * SUB_N,
+                    tma_load_2d(sB + (i * NSUB + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
                                 kEvictLast);
-            for (int kb = pre; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+            for (int i = pre; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
                 mbar_arrive_expect_tx(&full[s], stage_tx);
-                tma_load_2d(sA + s * A_BYTES, &tmW, &full[s], kb * BK, m0, kEvictFirst);
+                load_w(sA + s * A_BYTES, &tmW, &full[s], kb0 + i);
                 for (int j = 0; j < nb; ++j)
-                    tma_load_2d(sB + (s * NSUB + j) * B_BYTES, &tmX, &full[s], kb * BK, col0 + j * SUB_N,
+                    tma_load_2d(sB + (s * NSUB + j) * B_BYTES, &tmX, &full[s], (kb0 + i) * BK, col0 + j * SUB_N,
                                 kEvictLast);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_bf16(BM, SUB_N);
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&full[s], (kb / STAGES) & 1);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&full[s], (i / STAGES) & 1);
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA + s * A_BYTES);
                 const uint32_t b_base = smem_u32(sB + s * NSUB * B_BYTES);
@@ -167,7 +193,7 @@ __global__ void __launch_bounds__(256, 1)
                     const uint64_t adesc = umma_desc_k128(a_base + k * 32);
                     for (int j = 0; j < nb; ++j) {
                         const uint64_t bdesc = umma_desc_k128(b_base + j * B_BYTES + k * 32);
-                        tc_mma_bf16(tbase + j * SUB_N, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+                        tc_mma_bf16(tbase + j * SUB_N, adesc, bdesc, idesc, (i | k) != 0 ? 1u : 0u);
                     }
                 }
                 tc_commit(&empty[s]);   // frees the smem stage once these MMAs retire
@@ -176,37 +202,45 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         const int ew = warp - 4;       // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+        const int rl = ew * 32 + lane;
         pdl_wait();
         mbar_wait(tfull, 0);
         tc_fence_after();
-        const int row = m0 + ew * 32 + lane;
+        float* P = reinterpret_cast<float*>(smem);   // partial tile [col][128] (stages are idle now)
         for (int j = 0; j < nb; ++j) {
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + j * SUB_N + h * 32, r);
                 tc_wait_ld();
-                const int cbase = col0 + j * SUB_N + h * 32;
-                if (p.mode == kEpiQkvRope || p.mode == kEpiSwiglu) {
+                const int cl0 = j * SUB_N + h * 32;
+                if (S == 1) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const int col = cbase + c;
-                        if (col < p.ncols) {   // warp-uniform
-                            const float v = __uint_as_float(r[c]);
-                            const float partner = __shfl_xor_sync(0xffffffffu, v, 1);
-                            if (p.mode == kEpiQkvRope) epilogue_qkv(p, row, col, v, partner);
-                            else epilogue_swiglu(p, row, col, v, partner);
-                        }
-                    }
+                    for (int c = 0; c < 32; ++c)
+                        if (cl0 + c < ncols) epilogue_any(p, m0 + rl, col0 + cl0 + c, __uint_as_float(r[c]));
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const int col = cbase + c;
-                        if (col < p.ncols) epilogue_store(p, row, col, __uint_as_float(r[c]));
-                    }
+                    for (int c = 0; c < 32; ++c)
+                        if (cl0 + c < ncols) P[(cl0 + c) * BM + rl] = __uint_as_float(r[c]);
                 }
             }
         }
+    }
+    if (S > 1) {
+        cluster_sync_all();   // partial tiles of all segments visible cluster-wide
+        if (warp >= 4) {
+            const int rl = (warp - 4) * 32 + lane;
+            const uint32_t pbase = smem_u32(smem);
+            for (int cl = seg; cl < ncols; cl += S) {
+                float v[8];
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    v[s] = s < S ? ld_dsmem_f32(mapa_shared(pbase + 4u * static_cast<uint32_t>(cl * BM + rl), s))
+                                 : kNegZero;
+                epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v));
+            }
+        }
+        cluster_sync_all();   // peers keep their shared memory until every reader is done
     }
     tc_fence_before();
     __syncthreads();
@@ -243,19 +277,44 @@ cudaError_t launch_nsub(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.n_out / BM, (p.ncols + NSUB * SUB_N - 1) / (NSUB * SUB_N), 1);
+    cfg.gridDim = dim3(p.ksplit, p.n_out / BM, (p.ncols + NSUB * SUB_N - 1) / (NSUB * SUB_N));
     cfg.blockDim = dim3(256, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = p.ksplit;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<NSUB>, tmW, tmX, p);
 }
 
 }  // namespace
+
+bool make_tmap_weights(CUtensorMap* m, const void* ptr, uint64_t n_out, uint64_t k, bool tiled) {
+    EncodeFn enc = get_encode();
+    if (enc == nullptr) return false;
+    cuuint64_t dims[3];
+    cuuint64_t strides[2];
+    cuuint32_t box[3];
+    if (tiled) {   // [tiles*nkb][128 rows][64 k], each (tile, kb) block contiguous
+        dims[0] = 64; dims[1] = 128; dims[2] = (n_out / 128) * (k / 64);
+        strides[0] = 128; strides[1] = 128 * 128;
+        box[0] = 64; box[1] = 128; box[2] = 1;
+    } else {       // row-major [n_out][k] viewed as [n_out][k/64][64]
+        dims[0] = 64; dims[1] = k / 64; dims[2] = n_out;
+        strides[0] = 128; strides[1] = k * 2;
+        box[0] = 64; box[1] = 1; box[2] = 128;
+    }
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint32_t box_rows) {
     EncodeFn enc = get_encode();
@@ -271,9 +330,19 @@ bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ro
 
 // The sub-tile count only sizes the smem pipeline (deeper for small batches); the MMA shape, the
 // K order and each column's TMEM accumulation sequence are identical for every choice.
-cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p, cudaStream_t stream,
+int gemm_ksplit(int n_out, int k) {
+    const int tiles = n_out / BM, nkb = k / BK;
+    int s = 148 / (tiles > 0 ? tiles : 1);
+    s = s < 1 ? 1 : s;
+    s = s > 8 ? 8 : s;
+    return s > nkb ? nkb : s;
+}
+
+cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p_in, cudaStream_t stream,
                         bool pdl) {
-    if (p.n_out % BM != 0 || p.k % BK != 0 || p.k <= 0 || p.ncols <= 0) return cudaErrorInvalidValue;
+    if (p_in.n_out % BM != 0 || p_in.k % BK != 0 || p_in.k <= 0 || p_in.ncols <= 0) return cudaErrorInvalidValue;
+    GemmParams p = p_in;
+    p.ksplit = gemm_ksplit(p.n_out, p.k);
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
     if (p.ncols <= 128) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
     return launch_nsub<4>(tmW, tmX, p, stream, pdl);

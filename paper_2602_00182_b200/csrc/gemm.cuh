@@ -27,6 +27,8 @@ struct GemmParams {
     int k;       // reduction extent (multiple of 64)
     int ncols;   // number of activation columns
     int mode;
+    int ksplit;  // set by gemm_launch from the shape: fixed K-segments combined in segment order
+    int w_tiled; // weights pre-tiled [n_out/128][K/64][128][64] (engine) or plain row-major
     // kEpiStoreF32 / kEpiAddF32
     float* out;
     int64_t ld_out;            // per-column stride of `out` (elements)
@@ -49,8 +51,14 @@ struct GemmParams {
     __nv_bfloat16* act;        // [ncols][n_out/2]
 };
 
+// 3D tensor map of a weight matrix [n_out][k] (row-major view or pre-tiled, see gemm.cu load_w).
+bool make_tmap_weights(CUtensorMap* m, const void* ptr, uint64_t n_out, uint64_t k, bool tiled);
 // Tensor map for a row-major [rows, inner] bf16 matrix, box = 64 (inner) x box_rows, 128B swizzle.
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint32_t box_rows);
+
+// Number of fixed K-segments for a GEMM shape (part of the numeric definition):
+// S = min(8, K/64, max(1, 148 / (n_out/128))). Never depends on the batch.
+int gemm_ksplit(int n_out, int k);
 
 // Launch (PDL-enabled) on `stream`. tmW: box 128 rows; tmX: box 64 rows.
 cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p,

@@ -122,17 +122,21 @@ __global__ void __launch_bounds__(1024) tree_sum_kernel(const float* x, float* o
 // u = (z >> 40) * 2^-23 - 1 in [-1, 1) (prng.hpp:68-70 next_symmetric_f32); value u * 2^scale_exp
 // (exact) or, for norm gains, fma(u, 1/8, 1); stored as bf16 (RNE) at physical row r*row_mul+row_add.
 __global__ void init_kernel(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, float scale,
-                            int is_gamma, int row_mul, int row_add) {
+                            int is_gamma, int row_mul, int row_add, int tiled) {
     const int64_t n = rows * cols;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const uint64_t z = splitmix64_at(seed, static_cast<uint64_t>(i) + 1);
         const float u = __fsub_rn(__fmul_rn(static_cast<float>(z >> 40), 0x1.0p-23f), 1.0f);
         const float v = is_gamma ? __fmaf_rn(u, 0.125f, 1.0f) : __fmul_rn(u, scale);
         const int64_t r = i / cols, c = i % cols;
-        dst[(r * row_mul + row_add) * cols + c] = f2bf(v);
+        const int64_t pr = r * row_mul + row_add;
+        const int64_t o = tiled ? (((pr >> 7) * (cols >> 6) + (c >> 6)) * 128 + (pr & 127)) * 64 + (c & 63)
+                                : pr * cols + c;
+        dst[o] = f2bf(v);
     }
 }
 
+#if 0  // superseded by attention.cu
 // ------------------------------------------------------------------ attention
 // One CTA per (chunk, kv head, query column); G = hq/hkv query heads share the K/V chunk.
 //   s_p = tree_d(q_d * k_pd) * scale                 (products exact: bf16 x bf16)
@@ -162,29 +166,68 @@ __global__ void __launch_bounds__(128) attn_chunk_kernel(const AttnParams a, flo
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    for (int i = tid; i < G * HD; i += 128) sQ[i] = bf2f(qsrc[i]);
+    // K/V rows of this chunk: look up the (at most CH/page) page ids once, then stream all 16-byte
+    // vectors with cp.async (no dependent global round trip per row).
     constexpr int VPR = HD * 2 / 16;   // 16-byte vectors per row
-    for (int i = tid; i < n * VPR; i += 128) {
-        const int r = i / VPR, v = i % VPR;
-        const int p = p0 + r;
-        const int page_id = a.block_table[static_cast<int64_t>(slot) * a.max_pages + p / a.page];
-        const int64_t off = ((static_cast<int64_t>(page_id) * a.hkv + kvh) * a.page + p % a.page) * HD;
-        reinterpret_cast<int4*>(sK + r * HD)[v] = reinterpret_cast<const int4*>(a.kcache + off)[v];
-        reinterpret_cast<int4*>(sV + r * HD)[v] = reinterpret_cast<const int4*>(a.vcache + off)[v];
+    {
+        int pid[CH / 16];
+        const int npg = (n + a.page - 1) / a.page;
+        for (int j = 0; j < npg; ++j) pid[j] = a.block_table[static_cast<int64_t>(slot) * a.max_pages + (p0 / a.page) + j];
+        for (int i = tid; i < n * VPR; i += 128) {
+            const int r = i / VPR, v = i % VPR;
+            const int p = p0 + r;
+            const int64_t off = ((static_cast<int64_t>(pid[r / a.page]) * a.hkv + kvh) * a.page + p % a.page) * HD;
+            cp_async_16(sK + r * HD + v * 8, a.kcache + off + v * 8);
+            cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
+        }
+        cp_async_commit();
     }
+    for (int i = tid; i < G * HD; i += 128) sQ[i] = bf2f(qsrc[i]);
+    cp_async_wait_all();
     __syncthreads();
 
-    for (int p = warp; p < n; p += 4) {
-        float kv[E];
+    // scores: two positions per warp per iteration, all G heads, 2G interleaved butterflies
+    for (int p = warp * 2; p < n; p += 8) {
+        const bool two = p + 1 < n;
+        float kv0[E], kv1[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) kv[j] = bf2f(sK[p * HD + lane * E + j]);
-        for (int g = 0; g < G; ++g) {
-            float pr[E];
+        for (int j = 0; j < E; ++j) {
+            kv0[j] = bf2f(sK[p * HD + lane * E + j]);
+            kv1[j] = two ? bf2f(sK[(p + 1) * HD + lane * E + j]) : 0.0f;
+        }
+        float s0[8], s1[8];
 #pragma unroll
-            for (int j = 0; j < E; ++j) pr[j] = __fmul_rn(sQ[g * HD + lane * E + j], kv[j]);
-            float s = local_tree_sum<E>(pr);
-            s = warp_tree_sum(s);
-            if (lane == 0) sS[g * CH + p] = __fmul_rn(s, scale);
+        for (int g = 0; g < 8; ++g) {
+            if (g < G) {
+                float pr0[E], pr1[E];
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const float qv = sQ[g * HD + lane * E + j];
+                    pr0[j] = __fmul_rn(qv, kv0[j]);
+                    pr1[j] = __fmul_rn(qv, kv1[j]);
+                }
+                s0[g] = local_tree_sum<E>(pr0);
+                s1[g] = local_tree_sum<E>(pr1);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g < G) {
+                    s0[g] = __fadd_rn(s0[g], __shfl_xor_sync(0xffffffffu, s0[g], off));
+                    s1[g] = __fadd_rn(s1[g], __shfl_xor_sync(0xffffffffu, s1[g], off));
+                }
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g < G) {
+                    sS[g * CH + p] = __fmul_rn(s0[g], scale);
+                    if (two) sS[g * CH + p + 1] = __fmul_rn(s1[g], scale);
+                }
+            }
         }
     }
     __syncthreads();
@@ -215,44 +258,78 @@ __global__ void __launch_bounds__(128) attn_chunk_kernel(const AttnParams a, flo
     }
     __syncthreads();
 
-    float* ws = a.ws + ((static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks + c) * G * (HD + 2);
-    for (int idx = tid; idx < G * HD; idx += 128) {
-        const int g = idx / HD, dd = idx % HD;
-        float acc = 0.0f;
-        for (int p = 0; p < n; ++p) acc = __fmaf_rn(sS[g * CH + p], bf2f(sV[p * HD + dd]), acc);
-        ws[g * (HD + 2) + 2 + dd] = acc;
+    // o_d = fma chain over the chunk's positions in order; thread owns (d, heads g = t/HD + k*128/HD)
+    constexpr int GPT = (8 * HD + 127) / 128;   // max heads per thread
+    const int d = tid % HD, g0 = tid / HD, gstep = 128 / HD;
+    float acc[GPT];
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) acc[k] = 0.0f;
+#pragma unroll 4
+    for (int p = 0; p < n; ++p) {
+        const float v = bf2f(sV[p * HD + d]);
+#pragma unroll
+        for (int k = 0; k < GPT; ++k) {
+            const int g = g0 + k * gstep;
+            if (g < G) acc[k] = __fmaf_rn(sS[g * CH + p], v, acc[k]);
+        }
+    }
+    const int nch = (ctx + CH - 1) / CH;
+    __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    if (nch == 1) {
+        // single chunk: combine weight exp(0) == 1 exactly, so out = o / l directly
+#pragma unroll
+        for (int k = 0; k < GPT; ++k) {
+            const int g = g0 + k * gstep;
+            if (g < G) outp[g * HD + d] = f2bf(__fdiv_rn(__fmaf_rn(acc[k], 1.0f, 0.0f), __fmaf_rn(sL[g], 1.0f, 0.0f)));
+        }
+        return;
+    }
+    float* wsb = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2);
+    float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 2);
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = g0 + k * gstep;
+        if (g < G) ws[g * (HD + 2) + 2 + d] = acc[k];
     }
     if (tid < G) {
         ws[tid * (HD + 2)] = sM[tid];
         ws[tid * (HD + 2) + 1] = sL[tid];
     }
+    // The last chunk CTA of this (column, kv head) combines all chunks in chunk order. The ticket only
+    // elects the combiner; every value is combined in the same fixed order whoever arrives last.
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        int* t = a.tickets + static_cast<int64_t>(col) * a.hkv + kvh;
+        const int prev = atomicAdd(t, 1);
+        s_last = prev == nch - 1;
+        if (s_last) *t = 0;   // ready for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // out_d = bf16( (sum_c o_cd * a_c) / (sum_c l_c * a_c) ), a_c = exp(m_c - max_c m_c)
+    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = g0 + k * gstep;
+        if (g >= G) continue;
+        const float* base = wsb + g * (HD + 2);
+        float M = -FLT_MAX;
+        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(base + cc * cstride));
+        float L = 0.0f, O = 0.0f;
+        for (int cc = 0; cc < nch; ++cc) {
+            const float* w = base + cc * cstride;
+            const float al = det_expf(__fsub_rn(__ldcg(w), M));
+            L = __fmaf_rn(__ldcg(w + 1), al, L);
+            O = __fmaf_rn(__ldcg(w + 2 + d), al, O);
+        }
+        outp[g * HD + d] = f2bf(__fdiv_rn(O, L));
+    }
 }
 
-// out_d = bf16( (sum_c o_cd * a_c) / (sum_c l_c * a_c) ), a_c = exp(m_c - max_c m_c), chunk order.
-template <int HD>
-__global__ void __launch_bounds__(HD) attn_combine_kernel(const AttnParams a) {
-    pdl_trigger();
-    const int h = blockIdx.x, col = blockIdx.y;
-    pdl_wait();
-    const int pos = a.col_pos[col];
-    if (pos < 0) return;
-    const int G = a.hq / a.hkv;
-    const int kvh = h / G, g = h % G;
-    const int nch = (pos + kAttnChunk) / kAttnChunk;
-    const float* base = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2) + g * (HD + 2);
-    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
-    float M = -FLT_MAX;
-    for (int c = 0; c < nch; ++c) M = fmaxf(M, base[c * cstride]);
-    float L = 0.0f, O = 0.0f;
-    const int d = threadIdx.x;
-    for (int c = 0; c < nch; ++c) {
-        const float* w = base + c * cstride;
-        const float al = det_expf(__fsub_rn(w[0], M));
-        L = __fmaf_rn(w[1], al, L);
-        O = __fmaf_rn(w[2 + d], al, O);
-    }
-    a.out[static_cast<int64_t>(col) * a.hq * HD + h * HD + d] = f2bf(__fdiv_rn(O, L));
-}
+#endif
 
 // ------------------------------------------------------------------ softmax + decode
 // reference: det_softmax (detcore.cpp:187-198), decode_with_draw / decode_step (detcore.cpp:202-262)
@@ -598,40 +675,13 @@ cudaError_t launch_tree_sum(const float* x, float* out, int rows, int n, cudaStr
 }
 
 cudaError_t launch_init_tensor(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp,
-                               int is_gamma, int row_mul, int row_add, cudaStream_t stream) {
+                               int is_gamma, int row_mul, int row_add, cudaStream_t stream, bool tiled) {
     const float scale = ldexpf(1.0f, scale_exp);
     const int64_t n = rows * cols;
     const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 32));
-    init_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(dst, seed, rows, cols, scale, is_gamma, row_mul, row_add);
+    init_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(dst, seed, rows, cols, scale, is_gamma, row_mul, row_add,
+                                                             tiled ? 1 : 0);
     return cudaGetLastError();
-}
-
-size_t attn_workspace_bytes(const AttnParams& a) {
-    const int G = a.hq / a.hkv;
-    return sizeof(float) * static_cast<size_t>(a.ncols) * a.hkv * a.max_chunks * G * (a.hd + 2);
-}
-
-cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    if (a.hq % a.hkv != 0 || a.hq / a.hkv > 8) return cudaErrorInvalidValue;
-    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(a.hd)));
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attn_chunk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kAttnChunk * 128 * 2);
-        cudaFuncSetAttribute(attn_chunk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kAttnChunk * 64 * 2);
-        attr_set = true;
-    }
-    cudaLaunchAttribute attr[1];
-    const size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * a.hd * 2;
-    cudaLaunchConfig_t c1 = make_cfg(dim3(a.max_chunks, a.hkv, a.ncols), dim3(128), dsm, stream, attr, pdl);
-    cudaError_t e;
-    if (a.hd == 128) e = cudaLaunchKernelEx(&c1, attn_chunk_kernel<128>, a, scale);
-    else if (a.hd == 64) e = cudaLaunchKernelEx(&c1, attn_chunk_kernel<64>, a, scale);
-    else return cudaErrorInvalidValue;
-    if (e != cudaSuccess) return e;
-    cudaLaunchAttribute attr2[1];
-    cudaLaunchConfig_t c2 = make_cfg(dim3(a.hq, a.ncols), dim3(a.hd), 0, stream, attr2, pdl);
-    if (a.hd == 128) return cudaLaunchKernelEx(&c2, attn_combine_kernel<128>, a);
-    return cudaLaunchKernelEx(&c2, attn_combine_kernel<64>, a);
 }
 
 size_t sample_scratch_bytes(int rows, int vocab) { return sizeof(uint64_t) * static_cast<size_t>(rows) * vocab; }

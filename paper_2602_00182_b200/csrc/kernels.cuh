@@ -27,8 +27,9 @@ cudaError_t launch_rmsnorm_gather(const float* x, const __nv_bfloat16* gamma, __
                                   const int* out_index, int n, int d, float eps, cudaStream_t stream, bool pdl);
 cudaError_t launch_expf(const float* x, float* y, int64_t n, cudaStream_t stream);
 cudaError_t launch_tree_sum(const float* x, float* out, int rows, int n, cudaStream_t stream);
+// tiled: store GEMM-tiled [phys_rows/128][cols/64][128][64] instead of row-major
 cudaError_t launch_init_tensor(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int64_t cols, int scale_exp,
-                               int is_gamma, int row_mul, int row_add, cudaStream_t stream);
+                               int is_gamma, int row_mul, int row_add, cudaStream_t stream, bool tiled = false);
 
 // ---- attention ----
 struct AttnParams {
@@ -40,6 +41,7 @@ struct AttnParams {
     const int* col_req;            // slot of each column
     __nv_bfloat16* out;            // [ncols][hq*hd]
     float* ws;                     // partials
+    int* tickets;                  // [ncols][hkv], zero-initialised; reset by the combining CTA
     int ncols, hq, hkv, hd, page, max_pages, max_chunks;
 };
 size_t attn_workspace_bytes(const AttnParams& a);
