@@ -154,6 +154,10 @@ int detgpu_decode_exec_tuple(const uint8_t* bytes, size_t n, char* model_id, siz
 /* Y[col*ldy + n] = sum_k X[col*K + k] * W[n*K + k]; W [n_out,K] bf16, X [ncols,K] bf16. */
 int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy,
                   void* stream);
+/* Same with an explicit number of fixed K-segments (1..8; 0 = the engine's shape rule). Changes the
+ * numeric definition: measurement hook only. */
+int detgpu_k_gemm_split(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy,
+                        int ksplit, void* stream);
 /* out[col][i] = bf16(x[col][i] * rstd * gamma[i]); x f32 [ncols,d]; canonical-tree sum of squares. */
 int detgpu_k_rmsnorm(const float* x, const void* gamma, void* out, int ncols, int d, float eps, void* stream);
 /* f32 exp of n values with the engine's det_expf. */

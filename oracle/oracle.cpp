@@ -658,25 +658,30 @@ static float tc_dot(const uint16_t* w, const uint16_t* x, int K) {
     return c;
 }
 
-// The b200 GEMM splits K into S fixed segments (a function of the shape only; engine gemm.cu
-// gemm_ksplit): S = min(8, K/64, max(1, 148 / (rows/128))), segment s = 64-wide k-blocks
-// [s*nkb/S, (s+1)*nkb/S). Each segment is one tc_dot chain; the S partials are combined with the
-// reference tree in segment order.
-static int ksplit(int rows, int cols) {
-    const int tiles = rows / 128, nkb = cols / 64;
-    int s = 148 / (tiles > 0 ? tiles : 1);
-    s = std::max(1, std::min(8, s));
-    return std::min(s, std::max(nkb, 1));
-}
-static float tc_dot_segmented(const uint16_t* w, const uint16_t* x, int K, int S) {
-    if (S <= 1) return tc_dot(w, x, K);
-    const int nkb = K / 64;
-    float part[8];
-    for (int s = 0; s < S; ++s) {
-        const int k0 = (s * nkb / S) * 64, k1 = ((s + 1) * nkb / S) * 64;
-        part[s] = tc_dot(w + k0, x + k0, k1 - k0);
+// The b200 GEMM splits K into S fixed segments (engine gemm.cu gemm_ksplit):
+//   S = min(K/64, max(2, min(8, 256 / (rows/128)))), segment s = 64-wide k-blocks
+//   [s*nkb/S, (s+1)*nkb/S); each segment is one tc_dot chain, the S partials are combined with the
+//   reference tree in segment order. A function of (rows, K) only.
+struct Segs {
+    int n = 0;
+    int k0[8], k1[8];   // element ranges [k0, k1)
+};
+static Segs tile_segments(int rows, int cols, int /*tile*/) {
+    const int tiles = std::max(1, rows / 128), nkb = std::max(1, cols / 64);
+    const int S = std::min(nkb, std::max(2, std::min(8, 256 / tiles)));
+    Segs s;
+    for (int q = 0; q < S; ++q) {
+        s.k0[q] = (q * nkb / S) * 64;
+        s.k1[q] = ((q + 1) * nkb / S) * 64;
     }
-    return tree_reduce(part, size_t(S));
+    s.n = S;
+    return s;
+}
+static float tc_dot_segmented(const uint16_t* w, const uint16_t* x, const Segs& sg) {
+    if (sg.n == 1) return tc_dot(w + sg.k0[0], x + sg.k0[0], sg.k1[0] - sg.k0[0]);
+    float part[8];
+    for (int s = 0; s < sg.n; ++s) part[s] = tc_dot(w + sg.k0[s], x + sg.k0[s], sg.k1[s] - sg.k0[s]);
+    return tree_reduce(part, size_t(sg.n));
 }
 
 static int g_gemm_mode = 0;   // 0: b200 (tcgen05) profile ; 1: reference canonical tree
@@ -684,8 +689,9 @@ static int g_gemm_mode = 0;   // 0: b200 (tcgen05) profile ; 1: reference canoni
 // (detcore.cpp:180-181): products of two bf16 values are exact in f32, then the reference tree.
 static void gemv(const uint16_t* W, int rows, int cols, const uint16_t* x, float* y) {
     if (g_gemm_mode == 0) {
-        const int S = ksplit(rows, cols);
-        parallel_for(rows, [&](int64_t r) { y[r] = tc_dot_segmented(W + size_t(r) * cols, x, cols, S); });
+        std::vector<Segs> segs((rows + 127) / 128);
+        for (int t = 0; t < int(segs.size()); ++t) segs[t] = tile_segments(rows, cols, t);
+        parallel_for(rows, [&](int64_t r) { y[r] = tc_dot_segmented(W + size_t(r) * cols, x, segs[r / 128]); });
         return;
     }
     parallel_for(rows, [&](int64_t r) {

@@ -65,6 +65,7 @@ def _load() -> C.CDLL:
         "detgpu_decode_exec_tuple": (i32, [vp, sz, C.c_char_p, sz, vp, C.c_char_p, sz, C.c_char_p, sz,
                                            C.POINTER(Policy), C.POINTER(u64), vp, u32, C.POINTER(u32)]),
         "detgpu_k_gemm": (i32, [vp, vp, vp, i32, i32, i32, i64, vp]),
+        "detgpu_k_gemm_split": (i32, [vp, vp, vp, i32, i32, i32, i64, i32, vp]),
         "detgpu_k_rmsnorm": (i32, [vp, vp, vp, i32, i32, C.c_float, vp]),
         "detgpu_k_expf": (i32, [vp, vp, i64, vp]),
         "detgpu_k_tree_sum": (i32, [vp, vp, i32, i32, vp]),

@@ -33,6 +33,11 @@ const char* detgpu_version(void) { return "detgpu 0.1 (sm_100a, tcgen05)"; }
 const char* detgpu_global_error(void) { return detgpu::global_error().c_str(); }
 
 int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy, void* stream) {
+    return detgpu_k_gemm_split(W, X, Y, n_out, K, ncols, ldy, 0, stream);
+}
+
+int detgpu_k_gemm_split(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy, int ksplit,
+                        void* stream) {
     CUtensorMap tw, tx;
     if (!make_tmap_weights(&tw, W, n_out, K, false) || !make_tmap_bf16(&tx, X, K, ncols, 64)) {
         set_global_error("cuTensorMapEncodeTiled failed");
@@ -45,7 +50,9 @@ int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int 
     p.mode = kEpiStoreF32;
     p.out = Y;
     p.ld_out = ldy;
-    DETGPU_CUDA_TRY(gemm_launch(tw, tx, p, static_cast<cudaStream_t>(stream), false));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    p.ksplit = ksplit;
+    DETGPU_CUDA_TRY(gemm_launch(tw, tx, p, s, true));
     return DETGPU_OK;
 }
 

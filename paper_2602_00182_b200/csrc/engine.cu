@@ -62,7 +62,6 @@ struct Engine {
     int col_cap = 0;
     float* x = nullptr;
     __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *h_last = nullptr;
-    CUtensorMap tm_h, tm_attn, tm_act, tm_hlast;
     // KV cache (paged, static page ownership per slot)
     __nv_bfloat16 *kpool = nullptr, *vpool = nullptr;
     int pages_per_slot = 0, total_pages = 0, max_chunks = 0;
@@ -192,9 +191,6 @@ int init_buffers(Engine* E) {
     ENG_CUDA(cudaMemsetAsync(E->attn, 0, sizeof(__nv_bfloat16) * size_t(C) * qd, E->stream));
     ENG_CUDA(cudaMemsetAsync(E->act, 0, sizeof(__nv_bfloat16) * size_t(C) * c.F, E->stream));
     ENG_CUDA(cudaMemsetAsync(E->h_last, 0, sizeof(__nv_bfloat16) * size_t(B) * d, E->stream));
-    if (!make_tmap_bf16(&E->tm_h, E->h, d, C, 64) || !make_tmap_bf16(&E->tm_attn, E->attn, qd, C, 64) ||
-        !make_tmap_bf16(&E->tm_act, E->act, c.F, C, 64) || !make_tmap_bf16(&E->tm_hlast, E->h_last, d, B, 64))
-        return fail(E, DETGPU_ECUDA, "tensor map (activations)");
     // KV pool: static page ownership, slot b owns pages [b*pps, (b+1)*pps)
     E->pages_per_slot = (static_cast<int>(E->max_context) + kPage - 1) / kPage;
     E->total_pages = E->pages_per_slot * B;
@@ -215,6 +211,7 @@ int init_buffers(Engine* E) {
         a.max_chunks = E->max_chunks;
         ENG_CUDA(E->alloc(&E->attn_ws, attn_workspace_bytes(a) / sizeof(float)));
         ENG_CUDA(E->alloc(&E->attn_tickets, size_t(C) * c.hkv));
+
         ENG_CUDA(cudaMemset(E->attn_tickets, 0, sizeof(int) * size_t(C) * c.hkv));
     }
     // RoPE tables, host binary64 -> f32; identical expression in the oracle.
@@ -261,9 +258,10 @@ void mark(Engine* E, int cls) {
     cudaEventRecord(ev, E->stream);
     E->prof->push_back({ev, cls});
 }
-GemmParams gemm_base(int n_out, int k, int ncols) {
+GemmParams gemm_base(const Engine* E, int n_out, int k, int ncols) {
     GemmParams p{};
     p.w_tiled = 1;   // engine weights are stored pre-tiled
+
     p.n_out = n_out;
     p.k = k;
     p.ncols = ncols;
@@ -282,13 +280,18 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     const size_t per_layer = size_t(E->total_pages) * kPage * kd;
     cudaError_t e;
     uint64_t n = 0;
+    // activation tensor maps over exactly `ncols` rows: the MMA's padding rows are TMA zero-fill
+    CUtensorMap tm_h, tm_attn, tm_act;
+    if (!make_tmap_bf16(&tm_h, E->h, d, ncols, 64) || !make_tmap_bf16(&tm_attn, E->attn, qd, ncols, 64) ||
+        !make_tmap_bf16(&tm_act, E->act, c.F, ncols, 64))
+        return cudaErrorInvalidValue;
     e = launch_rmsnorm(nullptr, E->x, E->embed, tok, E->layers[0].attn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl);
     if (e != cudaSuccess) return e;
     mark(E, kProfNorm);
     ++n;
     for (int l = 0; l < c.L; ++l) {
         const Layer& Ly = E->layers[l];
-        GemmParams g = gemm_base(qd + 2 * kd, d, ncols);
+        GemmParams g = gemm_base(E, qd + 2 * kd, d, ncols);
         g.mode = kEpiQkvRope;
         g.q_out = E->q;
         g.hq = c.hq;
@@ -303,7 +306,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         g.block_table = E->block_table;
         g.max_pages = E->pages_per_slot;
         g.page = kPage;
-        if ((e = gemm_launch(Ly.tm_qkv, E->tm_h, g, s, pdl)) != cudaSuccess) return e;
+        if ((e = gemm_launch(Ly.tm_qkv, tm_h, g, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfQkv);
         AttnParams a{};
         a.q = E->q;
@@ -324,26 +327,26 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_chunks = E->max_chunks;
         if ((e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
-        GemmParams go = gemm_base(d, qd, ncols);
+        GemmParams go = gemm_base(E, d, qd, ncols);
         go.mode = kEpiAddF32;
         go.out = E->x;
         go.ld_out = d;
-        if ((e = gemm_launch(Ly.tm_o, E->tm_attn, go, s, pdl)) != cudaSuccess) return e;
+        if ((e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);
         if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl)) !=
             cudaSuccess)
             return e;
         mark(E, kProfNorm);
-        GemmParams gu = gemm_base(2 * c.F, d, ncols);
+        GemmParams gu = gemm_base(E, 2 * c.F, d, ncols);
         gu.mode = kEpiSwiglu;
         gu.act = E->act;
-        if ((e = gemm_launch(Ly.tm_gu, E->tm_h, gu, s, pdl)) != cudaSuccess) return e;
+        if ((e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfGateUp);
-        GemmParams gd = gemm_base(d, c.F, ncols);
+        GemmParams gd = gemm_base(E, d, c.F, ncols);
         gd.mode = kEpiAddF32;
         gd.out = E->x;
         gd.ld_out = d;
-        if ((e = gemm_launch(Ly.tm_down, E->tm_act, gd, s, pdl)) != cudaSuccess) return e;
+        if ((e = gemm_launch(Ly.tm_down, tm_act, gd, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfDown);
         n += 7;
         if (l + 1 < c.L) {
@@ -366,9 +369,11 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
 }
 
 // lm_head over `ncols` columns of X (tmX) into the trace at (slot, d_step[col]), then the sampler.
-cudaError_t head_and_sample(Engine* E, const CUtensorMap& tmX, int ncols, uint64_t* nlaunch) {
+cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64_t* nlaunch) {
     const ModelConfig& c = E->cfg;
-    GemmParams g = gemm_base(c.V, c.d, ncols);
+    CUtensorMap tmX;
+    if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
+    GemmParams g = gemm_base(E, c.V, c.d, ncols);
     g.mode = kEpiStoreF32;
     g.out = E->trace;
     g.col_step = E->d_step;
@@ -437,7 +442,7 @@ int get_graph(Engine* E, int ncols, cudaGraphExec_t* out) {
     ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
     uint64_t n = 0;
     cudaError_t e = forward(E, ncols, E->d_tok, E->d_pos, E->d_req, true, 0, &n);
-    if (e == cudaSuccess) e = head_and_sample(E, E->tm_h, ncols, &n);
+    if (e == cudaSuccess) e = head_and_sample(E, E->h, ncols, &n);
     cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
     ENG_CUDA(e);
     ENG_CUDA(e2);
@@ -547,7 +552,7 @@ int run_group(Engine* E, uint32_t n, const uint32_t* const* prompts, const uint3
         }
     }
     if (int rc = flush()) return rc;
-    ENG_CUDA(head_and_sample(E, E->tm_hlast, static_cast<int>(n), &nl));
+    ENG_CUDA(head_and_sample(E, E->h_last, static_cast<int>(n), &nl));
     ENG_CUDA(cudaEventRecord(E->ev[1], s));
     // decode loop: one graph replay per step
     cudaGraphExec_t gx = nullptr;
@@ -837,7 +842,7 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
         E->prof = &trail;
         mark(E, -1);
         err = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
-        if (err == cudaSuccess) err = head_and_sample(E, E->tm_h, static_cast<int>(ncols), nullptr);
+        if (err == cudaSuccess) err = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr);
         E->prof = nullptr;
         if (err == cudaSuccess) err = cudaStreamSynchronize(E->stream);
         for (size_t i = 1; i < trail.size() && err == cudaSuccess; ++i) {

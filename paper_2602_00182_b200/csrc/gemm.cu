@@ -21,13 +21,18 @@ constexpr int BK = 64;
 constexpr int SUB_N = 64;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int B_BYTES = SUB_N * BK * 2;     // 8 KB
-constexpr int TMEM_COLS = 256;
 
 template <int NSUB>
 struct Cfg {
+    // <= 128 columns: ~100 KB of shared memory so that two CTAs fit per SM (the next GEMM's CTAs,
+    // launched early by programmatic dependent launch, stream their weights while this one drains);
+    // 256-column tiles keep a deep ring at one CTA per SM.
     static constexpr int STAGE_BYTES = A_BYTES + NSUB * B_BYTES;
-    static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+    static constexpr int BUDGET = NSUB <= 2 ? 96 * 1024 : 192 * 1024;
+    static constexpr int STAGES = BUDGET / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int MIN_CTAS = NSUB <= 2 ? 2 : 1;
+    static constexpr uint32_t TMEM = NSUB * SUB_N;   // f32 accumulator columns (power of two)
 };
 
 __device__ __forceinline__ void epilogue_store(const GemmParams& p, int row, int col, float v) {
@@ -105,7 +110,7 @@ __device__ __forceinline__ void epilogue_any(const GemmParams& p, int row, int c
 // through distributed shared memory and combined per element with the reference tree over the S
 // partials in segment order (detcore.cpp:135-150). S depends only on the GEMM shape.
 template <int NSUB>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const GemmParams p) {
     using C = Cfg<NSUB>;
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(tfull, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tslot, TMEM_COLS);
+    if (warp == 2) tmem_alloc(tslot, C::TMEM);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tbase, TMEM_COLS);
+        tmem_dealloc(tbase, C::TMEM);
     }
 }
 
@@ -330,11 +335,13 @@ bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ro
 
 // The sub-tile count only sizes the smem pipeline (deeper for small batches); the MMA shape, the
 // K order and each column's TMEM accumulation sequence are identical for every choice.
+// S = min(K/64, max(2, min(8, 256 / tiles))): enough CTAs (with two resident per SM) to keep every
+// SM streaming weights; chosen from measured B200 scans (tools/gemm_split_scan.py).
 int gemm_ksplit(int n_out, int k) {
     const int tiles = n_out / BM, nkb = k / BK;
-    int s = 148 / (tiles > 0 ? tiles : 1);
-    s = s < 1 ? 1 : s;
+    int s = 256 / (tiles > 0 ? tiles : 1);
     s = s > 8 ? 8 : s;
+    s = s < 2 ? 2 : s;
     return s > nkb ? nkb : s;
 }
 
@@ -342,7 +349,8 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
                         bool pdl) {
     if (p_in.n_out % BM != 0 || p_in.k % BK != 0 || p_in.k <= 0 || p_in.ncols <= 0) return cudaErrorInvalidValue;
     GemmParams p = p_in;
-    p.ksplit = gemm_ksplit(p.n_out, p.k);
+    if (p.ksplit <= 0) p.ksplit = gemm_ksplit(p.n_out, p.k);
+    if (p.ksplit > 8 || p.ksplit > p.k / BK) return cudaErrorInvalidValue;
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
     if (p.ncols <= 128) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
     return launch_nsub<4>(tmW, tmX, p, stream, pdl);

@@ -27,7 +27,7 @@ struct GemmParams {
     int k;       // reduction extent (multiple of 64)
     int ncols;   // number of activation columns
     int mode;
-    int ksplit;  // set by gemm_launch from the shape: fixed K-segments combined in segment order
+    int ksplit;  // 0: gemm_ksplit(n_out, k) (the engine's numeric definition); >0: explicit (test hooks)
     int w_tiled; // weights pre-tiled [n_out/128][K/64][128][64] (engine) or plain row-major
     // kEpiStoreF32 / kEpiAddF32
     float* out;
@@ -57,10 +57,11 @@ bool make_tmap_weights(CUtensorMap* m, const void* ptr, uint64_t n_out, uint64_t
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint32_t box_rows);
 
 // Number of fixed K-segments for a GEMM shape (part of the numeric definition):
-// S = min(8, K/64, max(1, 148 / (n_out/128))). Never depends on the batch.
+// S = min(K/64, max(2, min(8, 256 / (n_out/128)))). Never depends on the batch.
 int gemm_ksplit(int n_out, int k);
 
-// Launch (PDL-enabled) on `stream`. tmW: box 128 rows; tmX: box 64 rows.
+// Launch (PDL-enabled) on `stream`. tmW: make_tmap_weights; tmX: box 64 rows over exactly ncols
+// rows, so the MMA's padding rows are TMA zero-fill and cost no memory traffic.
 cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p,
                         cudaStream_t stream, bool pdl);
 
