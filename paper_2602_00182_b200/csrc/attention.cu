@@ -36,9 +36,16 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __shared__ float sM[G], sL[G];
     __shared__ int s_last;
 
-    pdl_trigger();
     const int c = blockIdx.x, kvh = blockIdx.y, col = blockIdx.z;
-    pdl_wait();
+    // Decode: positions < pos were written by earlier steps and col_pos by the previous step's
+    // sampler; every kernel waits for its predecessor before triggering (gemm.cu), so both are
+    // complete when this kernel starts and the chunk's K/V can stream while the QKV GEMM (the
+    // predecessor, which appends position pos) is still running. Prefill reads K/V the predecessor
+    // writes, so it waits first.
+    if (!a.decode) {
+        pdl_wait();
+        pdl_trigger();
+    }
     const int pos = a.col_pos[col];
     if (pos < 0) return;
     const int ctx = pos + 1;
@@ -48,11 +55,11 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     const int slot = a.col_req[col];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // K/V rows: page ids of the chunk first, then every 16-byte vector with cp.async
+    // K/V rows: page ids of the chunk, then every 16-byte vector with cp.async
     constexpr int VPR = HD * 2 / 16;
-    {
-        const int* bt = a.block_table + static_cast<int64_t>(slot) * a.max_pages + p0 / a.page;
-        for (int i = tid; i < n * VPR; i += kNT) {
+    const int* bt = a.block_table + static_cast<int64_t>(slot) * a.max_pages + p0 / a.page;
+    auto load_rows = [&](int r_begin, int r_end) {
+        for (int i = r_begin * VPR + tid; i < r_end * VPR; i += kNT) {
             const int r = i / VPR, v = i % VPR;
             const int p = p0 + r;
             const int pid = __ldg(bt + r / a.page);
@@ -60,8 +67,16 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
             cp_async_16(sK + r * HD + v * 8, a.kcache + off + v * 8);
             cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
         }
-        cp_async_commit();
+    };
+    if (a.decode) {
+        load_rows(0, pos - p0 < n ? pos - p0 : n);   // history rows, before the wait
+        pdl_wait();
+        pdl_trigger();
+        if (pos - p0 < n) load_rows(pos - p0, n);     // the row the QKV GEMM just appended
+    } else {
+        load_rows(0, n);
     }
+    cp_async_commit();
     const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
     for (int i = tid; i < G * HD; i += kNT) sQ[i] = bf2f(qsrc[i]);
     cp_async_wait_all();

@@ -325,6 +325,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.page = kPage;
         a.max_pages = E->pages_per_slot;
         a.max_chunks = E->max_chunks;
+        a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
         if ((e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
         GemmParams go = gemm_base(E, d, qd, ncols);

@@ -150,8 +150,6 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tslot;
-    // Dependents only prefetch their own weights before griddepcontrol.wait, so they may launch now.
-    pdl_trigger();
 
     // Weight tile (128 rows x 64 k) through a 3D tensor map: pre-tiled weights are one contiguous
     // 16 KB block per (tile, k-block) -> coordinate (0, 0, tile*nkb + kb); a plain row-major matrix
@@ -160,16 +158,21 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         if (p.w_tiled) tma_load_3d(dst, m, bar, 0, 0, blockIdx.y * nkb_all + kb, kEvictFirst);
         else tma_load_3d(dst, m, bar, 0, kb, m0, kEvictFirst);
     };
+    const uint32_t stage_tx = A_BYTES + nb * B_BYTES;
+    const int pre = min(STAGES, nkb);
+    if (warp == 0 && lane == 0) {
+        // Weight tiles do not depend on the previous kernel: stream them before the PDL wait.
+        for (int i = 0; i < pre; ++i) {
+            mbar_arrive_expect_tx(&full[i], stage_tx);
+            load_w(sA + i * A_BYTES, &tmW, &full[i], kb0 + i);
+        }
+    }
+    // Every kernel waits for its predecessor before triggering its dependents, so when a kernel
+    // starts, all kernels before its predecessor have completed (attention relies on this).
+    pdl_wait();
+    pdl_trigger();
     if (warp == 0) {
         if (lane == 0) {
-            const uint32_t stage_tx = A_BYTES + nb * B_BYTES;
-            const int pre = min(STAGES, nkb);
-            // Weight tiles do not depend on the previous kernel: stream them before the PDL wait.
-            for (int i = 0; i < pre; ++i) {
-                mbar_arrive_expect_tx(&full[i], stage_tx);
-                load_w(sA + i * A_BYTES, &tmW, &full[i], kb0 + i);
-            }
-            pdl_wait();
             for (int i = 0; i < pre; ++i)
                 for (int j = 0; j < nb; ++j)
                     tma_load_2d(sB + (i * NSUB + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
@@ -208,7 +211,6 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     } else if (warp >= 4) {
         const int ew = warp - 4;       // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
         const int rl = ew * 32 + lane;
-        pdl_wait();
         mbar_wait(tfull, 0);
         tc_fence_after();
         float* P = reinterpret_cast<float*>(smem);   // partial tile [col][128] (stages are idle now)

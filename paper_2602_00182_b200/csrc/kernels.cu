@@ -60,8 +60,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       __nv_bfloat16* __restrict__ out, const int* __restrict__ col_index,
                                                       const int* __restrict__ out_index, int d, float eps) {
     __shared__ float scratch[32];
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     const int col = blockIdx.x;
     const int base = threadIdx.x * E;
     float v[E];
@@ -353,8 +353,8 @@ struct SampleSmem {
 
 __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
     __shared__ SampleSmem sm;
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int slot = r, step = 0;

@@ -43,6 +43,7 @@ struct AttnParams {
     float* ws;                     // partials
     int* tickets;                  // [ncols][hkv], zero-initialised; reset by the combining CTA
     int ncols, hq, hkv, hd, page, max_pages, max_chunks;
+    int decode;                    // 1: every column's positions < pos were written by earlier launches
 };
 size_t attn_workspace_bytes(const AttnParams& a);
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);
