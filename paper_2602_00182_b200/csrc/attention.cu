@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __syncthreads();
 
     // chunk softmax pieces: warp g owns head g (4 positions per lane)
+    const ExpTab tab = exp_tab_lane();
     for (int g = warp; g < G; g += kNW) {
         float sv[4], e[4];
         float m = -FLT_MAX;
@@ -142,7 +143,8 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int p = lane * 4 + j;
-            e[j] = p < n ? det_expf(__fsub_rn(sv[j], m)) : kNegZero;
+            const float ev = det_expf_shfl(p < n ? __fsub_rn(sv[j], m) : 0.0f, tab);
+            e[j] = p < n ? ev : kNegZero;
             sS[g * CH + p] = e[j];
         }
         float l = local_tree_sum<4>(e);
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         float L = 0.0f, O = 0.0f;
         for (int cc = 0; cc < nch; ++cc) {
             const float* w = base + cc * cstride;
-            const float al = det_expf(__fsub_rn(__ldcg(w), M));
+            const float al = det_expf_shfl(__fsub_rn(__ldcg(w), M), tab);
             L = __fmaf_rn(__ldcg(w + 1), al, L);
             O = __fmaf_rn(__ldcg(w + 2 + d), al, O);
         }

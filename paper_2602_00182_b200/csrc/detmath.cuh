@@ -56,6 +56,50 @@ __device__ __forceinline__ float det_expf(float x) {
     return __double2float_rn(y);
 }
 
+// The same function for warp-uniform call sites, with the 32-entry table held one entry per lane
+// and fetched by shuffle (a divergent __constant__ lookup serialises up to 32 ways). Every lane of
+// the warp must call it; the result is bit-identical to det_expf.
+struct ExpTab {
+    uint32_t lo, hi;
+};
+__device__ __forceinline__ ExpTab exp_tab_lane() {
+    const unsigned long long t = kExp2Tab[threadIdx.x & 31];
+    return ExpTab{static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32)};
+}
+__device__ __forceinline__ float det_expf_shfl(float x, ExpTab tab) {
+    const double InvLn2N = 0x1.71547652b82fep+0 * 32.0;
+    const double Shift = 0x1.8p+52;
+    const double C0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+    const double C1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+    const double C2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+    const double xd = static_cast<double>(x);
+    double kd = __fma_rn(InvLn2N, xd, Shift);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd = __dsub_rn(kd, Shift);
+    const double r = __fma_rn(InvLn2N, xd, -kd);
+    const int idx = static_cast<int>(ki & 31);
+    const uint32_t lo = __shfl_sync(0xffffffffu, tab.lo, idx);
+    const uint32_t hi = __shfl_sync(0xffffffffu, tab.hi, idx);
+    unsigned long long t = (static_cast<unsigned long long>(hi) << 32) | lo;
+    t += ki << 47;
+    const double s = __longlong_as_double(static_cast<long long>(t));
+    const double z = __fma_rn(C0, r, C1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(C2, r, 1.0);
+    y = __fma_rn(z, r2, y);
+    y = __dmul_rn(y, s);
+    float res = __double2float_rn(y);
+    const uint32_t ux = __float_as_uint(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    if (abstop >= 0x42b) {   // same special cases as det_expf, applied after the uniform shuffles
+        if (ux == 0xff800000u) res = 0.0f;
+        else if (abstop >= 0x7f8) res = x + x;
+        else if (x > 0x1.62e42ep6f) res = __int_as_float(0x7f800000);
+        else if (x < -0x1.9fe368p6f) res = 0.0f;
+    }
+    return res;
+}
+
 // ------------------------------------------------------------------ bf16
 __device__ __forceinline__ __nv_bfloat16 f2bf(float v) { return __float2bfloat16_rn(v); }
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }

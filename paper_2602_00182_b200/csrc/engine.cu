@@ -67,6 +67,7 @@ struct Engine {
     int pages_per_slot = 0, total_pages = 0, max_chunks = 0;
     int* block_table = nullptr;
     float* attn_ws = nullptr;
+    float* norm_ss = nullptr;   // [cols][d/128] per-tile sums of squares (fused-norm decode)
     int* attn_tickets = nullptr;
     float *rope_cos = nullptr, *rope_sin = nullptr;
     // prefill plan
@@ -211,6 +212,7 @@ int init_buffers(Engine* E) {
         a.max_chunks = E->max_chunks;
         ENG_CUDA(E->alloc(&E->attn_ws, attn_workspace_bytes(a) / sizeof(float)));
         ENG_CUDA(E->alloc(&E->attn_tickets, size_t(C) * c.hkv));
+        ENG_CUDA(E->alloc(&E->norm_ss, size_t(C) * (d / 128)));
 
         ENG_CUDA(cudaMemset(E->attn_tickets, 0, sizeof(int) * size_t(C) * c.hkv));
     }
@@ -285,7 +287,11 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     if (!make_tmap_bf16(&tm_h, E->h, d, ncols, 64) || !make_tmap_bf16(&tm_attn, E->attn, qd, ncols, 64) ||
         !make_tmap_bf16(&tm_act, E->act, c.F, ncols, 64))
         return cudaErrorInvalidValue;
-    e = launch_rmsnorm(nullptr, E->x, E->embed, tok, E->layers[0].attn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl);
+    // Decode with <= 8 columns: RMSNorm is fused into the consuming GEMMs (QKV, gate/up, lm_head),
+    // which build their B operand from the f32 residual stream; bits are identical.
+    const bool fuse = final_all && ncols <= 8;
+    e = launch_embed(E->embed, tok, E->x, fuse ? E->norm_ss : nullptr, E->layers[0].attn_norm, E->h, ncols, d, c.eps, s,
+                     pdl);
     if (e != cudaSuccess) return e;
     mark(E, kProfNorm);
     ++n;
@@ -306,6 +312,13 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         g.block_table = E->block_table;
         g.max_pages = E->pages_per_slot;
         g.page = kPage;
+        if (fuse) {
+            g.norm_x = E->x;
+            g.norm_ss = E->norm_ss;
+            g.norm_gamma = Ly.attn_norm;
+            g.norm_d = d;
+            g.norm_eps = c.eps;
+        }
         if ((e = gemm_launch(Ly.tm_qkv, tm_h, g, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfQkv);
         AttnParams a{};
@@ -332,25 +345,45 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         go.mode = kEpiAddF32;
         go.out = E->x;
         go.ld_out = d;
+        if (fuse) {
+            go.ss_out = E->norm_ss;
+            go.ss_tiles = d / 128;
+        }
         if ((e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);
-        if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s, pdl)) !=
-            cudaSuccess)
-            return e;
-        mark(E, kProfNorm);
+        if (!fuse) {
+            if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s,
+                                    pdl)) != cudaSuccess)
+                return e;
+            mark(E, kProfNorm);
+            ++n;
+        }
         GemmParams gu = gemm_base(E, 2 * c.F, d, ncols);
         gu.mode = kEpiSwiglu;
         gu.act = E->act;
+        if (fuse) {
+            gu.norm_x = E->x;
+            gu.norm_ss = E->norm_ss;
+            gu.norm_gamma = Ly.ffn_norm;
+            gu.norm_d = d;
+            gu.norm_eps = c.eps;
+        }
         if ((e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfGateUp);
         GemmParams gd = gemm_base(E, d, c.F, ncols);
         gd.mode = kEpiAddF32;
         gd.out = E->x;
         gd.ld_out = d;
+        if (fuse) {
+            gd.ss_out = E->norm_ss;
+            gd.ss_tiles = d / 128;
+        }
         if ((e = gemm_launch(Ly.tm_down, tm_act, gd, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfDown);
-        n += 7;
-        if (l + 1 < c.L) {
+        n += 6;
+        if (fuse) {
+            // norms fused into the next QKV GEMM / lm_head
+        } else if (l + 1 < c.L) {
             e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, E->layers[l + 1].attn_norm, E->h, nullptr, ncols, d,
                                c.eps, s, pdl);
             ++n;
@@ -363,19 +396,26 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             ++n;
         }
         if (e != cudaSuccess) return e;
-        mark(E, kProfNorm);
+        if (!fuse) mark(E, kProfNorm);
     }
     if (nlaunch) *nlaunch += n;
     return cudaSuccess;
 }
 
 // lm_head over `ncols` columns of X (tmX) into the trace at (slot, d_step[col]), then the sampler.
-cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64_t* nlaunch) {
+cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64_t* nlaunch, bool fuse_norm = false) {
     const ModelConfig& c = E->cfg;
     CUtensorMap tmX;
     if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
     GemmParams g = gemm_base(E, c.V, c.d, ncols);
     g.mode = kEpiStoreF32;
+    if (fuse_norm) {   // final RMSNorm fused into the lm_head's B operand (decode, <= 8 columns)
+        g.norm_x = E->x;
+        g.norm_ss = E->norm_ss;
+        g.norm_gamma = E->final_norm;
+        g.norm_d = c.d;
+        g.norm_eps = c.eps;
+    }
     g.out = E->trace;
     g.col_step = E->d_step;
     g.col_slot = E->d_req;
@@ -443,7 +483,7 @@ int get_graph(Engine* E, int ncols, cudaGraphExec_t* out) {
     ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
     uint64_t n = 0;
     cudaError_t e = forward(E, ncols, E->d_tok, E->d_pos, E->d_req, true, 0, &n);
-    if (e == cudaSuccess) e = head_and_sample(E, E->h, ncols, &n);
+    if (e == cudaSuccess) e = head_and_sample(E, E->h, ncols, &n, ncols <= 8);
     cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
     ENG_CUDA(e);
     ENG_CUDA(e2);
@@ -843,7 +883,7 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
         E->prof = &trail;
         mark(E, -1);
         err = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
-        if (err == cudaSuccess) err = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr);
+        if (err == cudaSuccess) err = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, ncols <= 8);
         E->prof = nullptr;
         if (err == cudaSuccess) err = cudaStreamSynchronize(E->stream);
         for (size_t i = 1; i < trail.size() && err == cudaSuccess; ++i) {

@@ -35,7 +35,7 @@ struct Cfg {
     static constexpr uint32_t TMEM = NSUB * SUB_N;   // f32 accumulator columns (power of two)
 };
 
-__device__ __forceinline__ void epilogue_store(const GemmParams& p, int row, int col, float v) {
+__device__ __forceinline__ float epilogue_store(const GemmParams& p, int row, int col, float v) {
     switch (p.mode) {
         case kEpiStoreF32: {
             int64_t off;
@@ -47,15 +47,16 @@ __device__ __forceinline__ void epilogue_store(const GemmParams& p, int row, int
                 off = static_cast<int64_t>(col) * p.ld_out;
             }
             p.out[off + row] = v;
-            return;
+            return v;
         }
         case kEpiAddF32: {
             float* dst = p.out + static_cast<int64_t>(col) * p.ld_out + row;
-            *dst = __fadd_rn(*dst, v);
-            return;
+            const float r = __fadd_rn(*dst, v);
+            *dst = r;
+            return r;
         }
         default:
-            return;
+            return v;
     }
 }
 
@@ -87,20 +88,144 @@ __device__ __forceinline__ void epilogue_qkv(const GemmParams& p, int row, int c
 }
 
 // silu(g) * u with g = gate row 2j, u = up row 2j+1; silu(g) = g / (1 + exp(-g)).
-__device__ __forceinline__ void epilogue_swiglu(const GemmParams& p, int row, int col, float v, float partner) {
+__device__ __forceinline__ void epilogue_swiglu(const GemmParams& p, int row, int col, float v, float partner,
+                                                float e /* det_expf(-v) */) {
     if ((row & 1) != 0) return;
-    const float e = det_expf(-v);
     const float sg = __fdiv_rn(v, __fadd_rn(1.0f, e));
     p.act[static_cast<int64_t>(col) * (p.n_out / 2) + (row >> 1)] = f2bf(__fmul_rn(sg, partner));
 }
 
-__device__ __forceinline__ void epilogue_any(const GemmParams& p, int row, int col, float v) {
+__device__ __forceinline__ float epilogue_any(const GemmParams& p, int row, int col, float v, ExpTab tab) {
     if (p.mode == kEpiQkvRope || p.mode == kEpiSwiglu) {
         const float partner = __shfl_xor_sync(0xffffffffu, v, 1);   // callers keep `col` warp-uniform
         if (p.mode == kEpiQkvRope) epilogue_qkv(p, row, col, v, partner);
-        else epilogue_swiglu(p, row, col, v, partner);
-    } else {
-        epilogue_store(p, row, col, v);
+        else epilogue_swiglu(p, row, col, v, partner, det_expf_shfl(-v, tab));   // all lanes
+        return v;
+    }
+    return epilogue_store(p, row, col, v);
+}
+
+__device__ __forceinline__ void epi_bar();
+
+// Sum of squares of the updated residual over this tile's 128 rows for one column (perfect tree:
+// lane butterfly over 32 consecutive rows, then the 4 warps), stored as the tile's partial of the
+// next RMSNorm. All 128 epilogue threads call it with the same column.
+__device__ __forceinline__ void tile_sumsq(const GemmParams& p, int tile, int col, float xnew, int ew, int lane,
+                                           float* s_red) {
+    float q = warp_tree_sum(__fmul_rn(xnew, xnew));
+    if (lane == 0) s_red[ew] = q;
+    epi_bar();
+    if (ew == 0 && lane == 0)
+        p.ss_out[static_cast<int64_t>(col) * p.ss_tiles + tile] =
+            __fadd_rn(__fadd_rn(s_red[0], s_red[1]), __fadd_rn(s_red[2], s_red[3]));
+    epi_bar();
+}
+
+// Perfect-tree sum of squares of a row of d = 32*E floats (lane owns E contiguous): float4 chunks
+// merged with a binary counter, then the lane butterfly == the canonical tree over d.
+template <int E>
+__device__ __forceinline__ float warp_sumsq(const float* __restrict__ row, int lane) {
+    constexpr int NC = E / 4;
+    constexpr int DEPTH = (NC >= 32 ? 5 : NC >= 16 ? 4 : NC >= 8 ? 3 : NC >= 4 ? 2 : NC >= 2 ? 1 : 0) + 1;
+    float stack[DEPTH];
+    const float4* src = reinterpret_cast<const float4*>(row + lane * E);
+#pragma unroll
+    for (int g = 0; g < NC; ++g) {
+        const float4 v = src[g];
+        float q[4] = {__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y), __fmul_rn(v.z, v.z), __fmul_rn(v.w, v.w)};
+        float carry = local_tree_sum<4>(q);
+        int lvl = 0;
+#pragma unroll
+        for (int b = g; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stack[lvl], carry);
+        stack[lvl] = carry;
+    }
+    return warp_tree_sum(stack[DEPTH - 1]);
+}
+
+__device__ __forceinline__ float norm_sumsq(const float* row, int d, int lane) {
+    switch (d) {
+        case 256: return warp_sumsq<8>(row, lane);
+        case 512: return warp_sumsq<16>(row, lane);
+        case 1024: return warp_sumsq<32>(row, lane);
+        case 2048: return warp_sumsq<64>(row, lane);
+        default: return warp_sumsq<128>(row, lane);   // 4096
+    }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Epilogue warps as the B-operand producer: rstd per column, then for every k-block of the segment
+// bf16((x * rstd) * gamma) written straight into the stage's 128B-swizzled K-major tile (row = col,
+// 16-byte chunk j of the 128-byte row stored at chunk j ^ (row % 8)). Rows >= ncols are left as
+// they are: MMA columns are independent, and those columns are never stored.
+template <int STAGES>
+__device__ void norm_b_producer(const GemmParams& p, uint8_t* sB, uint64_t* full, uint64_t* empty, int kb0, int nkb,
+                                int col0, int ncols, int ew, int lane) {
+    __shared__ float s_rstd[8];
+    const int d = p.norm_d;
+    const int t = ew * 32 + lane;
+    const int c = t >> 4, kq = (t & 15) * 4;   // column, first of 4 consecutive k in the block
+    const bool active = c < ncols;
+    const float* xrow = p.norm_x + static_cast<int64_t>(col0 + (active ? c : 0)) * d + kq;
+    const __nv_bfloat16* grow = p.norm_gamma + kq;
+    // software pipeline: the x / gamma values of the next PF k-blocks are in flight in registers
+    // (issued before the rstd reduction so both latencies overlap)
+    constexpr int PF = 8;
+    float4 xr[PF];
+    uint2 gr[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        if (active && j < nkb) {
+            xr[j] = *reinterpret_cast<const float4*>(xrow + (kb0 + j) * BK);
+            gr[j] = *reinterpret_cast<const uint2*>(grow + (kb0 + j) * BK);
+        }
+    }
+    const int ntiles = d / 128;
+    for (int cc = ew; cc < ncols; cc += 4) {
+        // the producer of x left one partial per 128-row tile; their tree is the tree over d
+        const float part = lane < ntiles ? p.norm_ss[static_cast<int64_t>(col0 + cc) * ntiles + lane] : kNegZero;
+        const float ss = warp_tree_sum(part);
+        if (lane == 0) {
+            const float ms = __fdiv_rn(ss, static_cast<float>(d));
+            s_rstd[cc] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, p.norm_eps)));
+        }
+    }
+    epi_bar();
+    const float rstd = active ? s_rstd[c] : 0.0f;
+    for (int i0 = 0; i0 < nkb; i0 += PF) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const int i = i0 + j;
+            if (i >= nkb) break;   // uniform across the 128 producer threads
+            const int s = i % STAGES;
+            uint2 packed = make_uint2(0u, 0u);
+            if (active) {
+                const float4 xv = xr[j];
+                const uint2 gv = gr[j];
+                if (i + PF < nkb) {
+                    xr[j] = *reinterpret_cast<const float4*>(xrow + (kb0 + i + PF) * BK);
+                    gr[j] = *reinterpret_cast<const uint2*>(grow + (kb0 + i + PF) * BK);
+                }
+                const float g0 = __uint_as_float(gv.x << 16), g1 = __uint_as_float(gv.x & 0xffff0000u);
+                const float g2 = __uint_as_float(gv.y << 16), g3 = __uint_as_float(gv.y & 0xffff0000u);
+                const __nv_bfloat16 h0 = f2bf(__fmul_rn(__fmul_rn(xv.x, rstd), g0));
+                const __nv_bfloat16 h1 = f2bf(__fmul_rn(__fmul_rn(xv.y, rstd), g1));
+                const __nv_bfloat16 h2 = f2bf(__fmul_rn(__fmul_rn(xv.z, rstd), g2));
+                const __nv_bfloat16 h3 = f2bf(__fmul_rn(__fmul_rn(xv.w, rstd), g3));
+                packed.x = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+                           (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+                packed.y = static_cast<uint32_t>(__bfloat16_as_ushort(h2)) |
+                           (static_cast<uint32_t>(__bfloat16_as_ushort(h3)) << 16);
+            }
+            if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            if (active) {
+                const int chunk = (kq >> 3) ^ (c & 7);
+                *reinterpret_cast<uint2*>(sB + s * B_BYTES + c * 128 + chunk * 16 + (kq & 7) * 2) = packed;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+            epi_bar();
+            if (t == 0) mbar_arrive(&full[s]);
+        }
     }
 }
 
@@ -124,6 +249,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     uint64_t* tfull = empty + STAGES;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
 
+    __shared__ float s_red[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.ksplit;
     const int seg = blockIdx.x;                 // == %cluster_ctarank
@@ -134,12 +260,16 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     const int nkb_all = p.k / BK;
     const int kb0 = seg * nkb_all / S, kb1 = (seg + 1) * nkb_all / S;
     const int nkb = kb1 - kb0;
+    // Fused RMSNorm (decode, <= 8 columns): the B operand is produced in shared memory by the
+    // epilogue warps from the f32 residual stream instead of being loaded by TMA from a separately
+    // normalised bf16 copy; bits are identical to rmsnorm_kernel + TMA.
+    const bool fused = p.norm_x != nullptr;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmX);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], fused ? 2 : 1);   // fused norm: TMA (A) + software producer (B)
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
@@ -158,7 +288,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         if (p.w_tiled) tma_load_3d(dst, m, bar, 0, 0, blockIdx.y * nkb_all + kb, kEvictFirst);
         else tma_load_3d(dst, m, bar, 0, kb, m0, kEvictFirst);
     };
-    const uint32_t stage_tx = A_BYTES + nb * B_BYTES;
+    const uint32_t stage_tx = fused ? A_BYTES : A_BYTES + nb * B_BYTES;
     const int pre = min(STAGES, nkb);
     if (warp == 0 && lane == 0) {
         // Weight tiles do not depend on the previous kernel: stream them before the PDL wait.
@@ -173,18 +303,20 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     pdl_trigger();
     if (warp == 0) {
         if (lane == 0) {
-            for (int i = 0; i < pre; ++i)
-                for (int j = 0; j < nb; ++j)
-                    tma_load_2d(sB + (i * NSUB + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
-                                kEvictLast);
+            if (!fused)
+                for (int i = 0; i < pre; ++i)
+                    for (int j = 0; j < nb; ++j)
+                        tma_load_2d(sB + (i * NSUB + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
+                                    kEvictLast);
             for (int i = pre; i < nkb; ++i) {
                 const int s = i % STAGES;
                 mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
                 mbar_arrive_expect_tx(&full[s], stage_tx);
                 load_w(sA + s * A_BYTES, &tmW, &full[s], kb0 + i);
-                for (int j = 0; j < nb; ++j)
-                    tma_load_2d(sB + (s * NSUB + j) * B_BYTES, &tmX, &full[s], (kb0 + i) * BK, col0 + j * SUB_N,
-                                kEvictLast);
+                if (!fused)
+                    for (int j = 0; j < nb; ++j)
+                        tma_load_2d(sB + (s * NSUB + j) * B_BYTES, &tmX, &full[s], (kb0 + i) * BK,
+                                    col0 + j * SUB_N, kEvictLast);
             }
         }
     } else if (warp == 1) {
@@ -211,6 +343,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     } else if (warp >= 4) {
         const int ew = warp - 4;       // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
         const int rl = ew * 32 + lane;
+        const ExpTab tab = exp_tab_lane();
+        if (fused) norm_b_producer<STAGES>(p, sB, full, empty, kb0, nkb, col0, ncols, ew, lane);
         mbar_wait(tfull, 0);
         tc_fence_after();
         float* P = reinterpret_cast<float*>(smem);   // partial tile [col][128] (stages are idle now)
@@ -224,7 +358,10 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 if (S == 1) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                        if (cl0 + c < ncols) epilogue_any(p, m0 + rl, col0 + cl0 + c, __uint_as_float(r[c]));
+                        if (cl0 + c < ncols) {
+                            const float xn = epilogue_any(p, m0 + rl, col0 + cl0 + c, __uint_as_float(r[c]), tab);
+                            if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl0 + c, xn, ew, lane, s_red);
+                        }
                 } else {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
@@ -237,6 +374,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         cluster_sync_all();   // partial tiles of all segments visible cluster-wide
         if (warp >= 4) {
             const int rl = (warp - 4) * 32 + lane;
+            const ExpTab tab = exp_tab_lane();
             const uint32_t pbase = smem_u32(smem);
             for (int cl = seg; cl < ncols; cl += S) {
                 float v[8];
@@ -244,7 +382,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 for (int s = 0; s < 8; ++s)
                     v[s] = s < S ? ld_dsmem_f32(mapa_shared(pbase + 4u * static_cast<uint32_t>(cl * BM + rl), s))
                                  : kNegZero;
-                epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v));
+                const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v), tab);
+                if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, warp - 4, lane, s_red);
             }
         }
         cluster_sync_all();   // peers keep their shared memory until every reader is done
@@ -353,6 +492,11 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     GemmParams p = p_in;
     if (p.ksplit <= 0) p.ksplit = gemm_ksplit(p.n_out, p.k);
     if (p.ksplit > 8 || p.ksplit > p.k / BK) return cudaErrorInvalidValue;
+    if (p.norm_x != nullptr && (p.ncols > 8 || p.norm_ss == nullptr || p.k != p.norm_d || (p.norm_d & (p.norm_d - 1)) != 0 ||
+                                p.norm_d < 256 || p.norm_d > 4096))
+        return cudaErrorInvalidValue;
+    if (p.ss_out != nullptr && (p.mode != kEpiAddF32 || p.n_out != p.ss_tiles * BM || p.ncols > 8))
+        return cudaErrorInvalidValue;
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
     if (p.ncols <= 128) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
     return launch_nsub<4>(tmW, tmX, p, stream, pdl);

@@ -49,6 +49,15 @@ struct GemmParams {
     int page;                  // positions per page
     // kEpiSwiglu
     __nv_bfloat16* act;        // [ncols][n_out/2]
+    // fused RMSNorm of the B operand (<= 8 columns, K == norm_d): X = bf16(rmsnorm(norm_x) * gamma)
+    const float* norm_x;       // [ncols][norm_d] f32 residual stream, or nullptr (X via tmX)
+    const float* norm_ss;      // [ncols][norm_d/128] per-tile sums of squares of norm_x
+    const __nv_bfloat16* norm_gamma;
+    int norm_d;
+    float norm_eps;
+    // kEpiAddF32 in fused decode: emit the next RMSNorm's per-tile sums of squares of the result
+    float* ss_out;             // [ncols][ss_tiles] or nullptr
+    int ss_tiles;              // n_out / 128
 };
 
 // 3D tensor map of a weight matrix [n_out][k] (row-major view or pre-tiled, see gemm.cu load_w).

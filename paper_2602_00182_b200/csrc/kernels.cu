@@ -21,6 +21,7 @@ __device__ __forceinline__ int next_pow2(int n) {
 }
 
 // Perfect tree over [0, n) padded with -0 to P2 = max(128, pow2 >= n): 128-element tiles reduced by
+// (ld(i, valid) must return -0.0f for !valid)
 // one warp each (4 consecutive per lane, then the lane butterfly), tile sums reduced level by level
 // in shared memory. Requires blockDim.x == 1024 and n <= 131072.
 template <class Load>
@@ -33,7 +34,7 @@ __device__ float block_tree_sum_1024(int n, Load ld, float* s_tiles) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int i = t * 128 + lane * 4 + j;
-            v[j] = i < n ? ld(i) : kNegZero;
+            v[j] = ld(i, i < n);   // called by every lane (warp-uniform), returns -0 when !valid
         }
         float s = local_tree_sum<4>(v);
         s = warp_tree_sum(s);
@@ -58,7 +59,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       const int* __restrict__ col_token,
                                                       const __nv_bfloat16* __restrict__ gamma,
                                                       __nv_bfloat16* __restrict__ out, const int* __restrict__ col_index,
-                                                      const int* __restrict__ out_index, int d, float eps) {
+                                                      const int* __restrict__ out_index, int d, float eps,
+                                                      float* __restrict__ ss_out) {
     __shared__ float scratch[32];
     pdl_wait();
     pdl_trigger();
@@ -73,6 +75,19 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
         float* dst = x_out + static_cast<int64_t>(col) * d + base;
 #pragma unroll
         for (int j = 0; j < E; ++j) dst[j] = v[j];
+        if (ss_out != nullptr) {
+            // per-128-element partial sums of squares of the new residual row (fused-norm decode):
+            // warp w reduces tiles w, w+8, ... with 4 contiguous elements per lane + the butterfly
+            __syncthreads();
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const float* xr = x_out + static_cast<int64_t>(col) * d;
+            for (int t = warp; t < d / 128; t += 8) {
+                const float4 f = *reinterpret_cast<const float4*>(xr + t * 128 + lane * 4);
+                float q[4] = {__fmul_rn(f.x, f.x), __fmul_rn(f.y, f.y), __fmul_rn(f.z, f.z), __fmul_rn(f.w, f.w)};
+                const float tsum = warp_tree_sum(local_tree_sum<4>(q));
+                if (lane == 0) ss_out[static_cast<int64_t>(col) * (d / 128) + t] = tsum;
+            }
+        }
     } else {
         const int row = col_index != nullptr ? col_index[col] : col;
         const float* src = x_in + static_cast<int64_t>(row) * d + base;
@@ -105,15 +120,25 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 }
 
 // ------------------------------------------------------------------ misc test kernels
+// Both exp variants; a disagreement between them is reported as the NaN payload 0x7fc00bad.
 __global__ void expf_kernel(const float* x, float* y, int64_t n) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-        y[i] = det_expf(x[i]);
+    const ExpTab tab = exp_tab_lane();
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const float xv = i < n ? x[i] : 0.0f;
+        const float a = det_expf_shfl(xv, tab);   // warp-uniform loop: every lane calls
+        if (i < n) {
+            const float b = det_expf(xv);
+            y[i] = __float_as_uint(a) == __float_as_uint(b) ? a : __uint_as_float(0x7fc00badu);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(1024) tree_sum_kernel(const float* x, float* out, int n) {
     __shared__ float tiles[1024];
     const float* row = x + static_cast<int64_t>(blockIdx.x) * n;
-    const float s = block_tree_sum_1024(n, [&](int i) { return row[i]; }, tiles);
+    const float s = block_tree_sum_1024(n, [&](int i, bool ok) { return ok ? row[i] : kNegZero; }, tiles);
     if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
@@ -424,10 +449,12 @@ __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
     }
 
     // pass 2: e_i = exp(l_i - max); S = canonical tree of e
+    const ExpTab tab = exp_tab_lane();
     const float S = block_tree_sum_1024(
         V,
-        [&](int i) {
-            const float e = det_expf(__fsub_rn(L[i], maxv));
+        [&](int i, bool ok) {
+            const float e = det_expf_shfl(ok ? __fsub_rn(L[i], maxv) : 0.0f, tab);
+            if (!ok) return kNegZero;
             P[i] = e;
             return e;
         },
@@ -577,7 +604,8 @@ __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
             __syncthreads();
         }
         // renormalise with the canonical tree over the kept prefix, in sorted order
-        const float mass = block_tree_sum_1024(kept, [&](int i) { return key_prob(sorted[i]); }, sm.tiles);
+        const float mass =
+            block_tree_sum_1024(kept, [&](int i, bool ok) { return ok ? key_prob(sorted[i]) : kNegZero; }, sm.tiles);
         if (tid == 0) {
             if (!(mass > 0.0f)) {
                 err = DETGPU_EINVAL;
@@ -634,24 +662,31 @@ cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16*
     return launch_rmsnorm_ex(x_in, x_out, embed, col_token, gamma, out, col_index, nullptr, ncols, d, eps, stream, pdl);
 }
 
+cudaError_t launch_embed(const __nv_bfloat16* embed, const int* col_token, float* x_out, float* ss_out,
+                         const __nv_bfloat16* gamma, __nv_bfloat16* h_out, int ncols, int d, float eps,
+                         cudaStream_t stream, bool pdl) {
+    return launch_rmsnorm_ex(nullptr, x_out, embed, col_token, gamma, h_out, nullptr, nullptr, ncols, d, eps, stream, pdl,
+                             ss_out);
+}
+
 cudaError_t launch_rmsnorm_ex(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
                               const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index, const int* out_index,
-                              int ncols, int d, float eps, cudaStream_t stream, bool pdl) {
+                              int ncols, int d, float eps, cudaStream_t stream, bool pdl, float* ss_out) {
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = make_cfg(dim3(ncols), dim3(256), 0, stream, attr, pdl);
     const int* ii = in_index;
     const int* oi = out_index;
     switch (d) {
         case 256:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<1>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<1>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps, ss_out);
         case 512:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<2>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<2>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps, ss_out);
         case 1024:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<4>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<4>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps, ss_out);
         case 2048:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<8>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<8>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps, ss_out);
         case 4096:
-            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<16>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps);
+            return cudaLaunchKernelEx(&cfg, rmsnorm_kernel<16>, x_in, x_out, embed, col_token, gamma, out, ii, oi, d, eps, ss_out);
         default:
             return cudaErrorInvalidValue;
     }

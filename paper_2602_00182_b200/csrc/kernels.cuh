@@ -21,7 +21,12 @@ cudaError_t launch_rmsnorm(const float* x_in, float* x_out, const __nv_bfloat16*
 
 cudaError_t launch_rmsnorm_ex(const float* x_in, float* x_out, const __nv_bfloat16* embed, const int* col_token,
                               const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index, const int* out_index,
-                              int ncols, int d, float eps, cudaStream_t stream, bool pdl);
+                              int ncols, int d, float eps, cudaStream_t stream, bool pdl, float* ss_out = nullptr);
+// Embedding gather x = embed[tok] (+ normalised h); with ss_out also the per-128-element partial
+// sums of squares of x that a fused-norm GEMM consumes.
+cudaError_t launch_embed(const __nv_bfloat16* embed, const int* col_token, float* x_out, float* ss_out,
+                         const __nv_bfloat16* gamma, __nv_bfloat16* h_out, int ncols, int d, float eps,
+                         cudaStream_t stream, bool pdl);
 // out[out_index[i]] = rmsnorm(x[in_index[i]]) for i < n
 cudaError_t launch_rmsnorm_gather(const float* x, const __nv_bfloat16* gamma, __nv_bfloat16* out, const int* in_index,
                                   const int* out_index, int n, int d, float eps, cudaStream_t stream, bool pdl);
