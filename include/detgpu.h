@@ -124,6 +124,11 @@ void* detgpu_stream(const detgpu_engine* h);
 int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t reps,
                                float* ms_by_class, uint32_t* launches_by_class);
 
+/* Timing experiment: mean ms of a captured decode-step graph with the kernel classes of skip_mask
+ * left out (results meaningless when skip_mask != 0). Measurement hook only. */
+int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t skip_mask, uint32_t reps,
+                         float* ms_per_step);
+
 /* ---- host-side helpers of the receipt path (no GPU needed) ---- */
 
 /* SHA-256 (receipts.hpp:53-54 hash_commit; sha256.cpp:32-37). */

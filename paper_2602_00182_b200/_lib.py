@@ -57,6 +57,7 @@ def _load() -> C.CDLL:
                                   C.POINTER(C.c_uint8), u32, C.POINTER(Stats)]),
         "detgpu_stream": (vp, [vp]),
         "detgpu_profile_decode_step": (i32, [vp, u32, u32, u32, C.POINTER(C.c_float), C.POINTER(u32)]),
+        "detgpu_profile_graph": (i32, [vp, u32, u32, u32, u32, C.POINTER(C.c_float)]),
         "detgpu_sha256": (None, [vp, sz, vp]),
         "detgpu_canonical_size": (sz, [u32, u32]),
         "detgpu_encode_canonical": (None, [vp, u32, vp, u32, vp]),

@@ -97,6 +97,7 @@ struct Engine {
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<std::pair<cudaEvent_t, int>>* prof = nullptr;
+    unsigned skip_mask = 0;   // timing experiments only (detgpu_profile_graph): kernel classes left out
 
     template <class T>
     cudaError_t alloc(T** p, size_t count) {
@@ -319,7 +320,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             g.norm_d = d;
             g.norm_eps = c.eps;
         }
-        if ((e = gemm_launch(Ly.tm_qkv, tm_h, g, s, pdl)) != cudaSuccess) return e;
+        if (!(E->skip_mask & (1u << kProfQkv)) && (e = gemm_launch(Ly.tm_qkv, tm_h, g, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfQkv);
         AttnParams a{};
         a.q = E->q;
@@ -339,7 +340,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_pages = E->pages_per_slot;
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
-        if ((e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
+        if (!(E->skip_mask & (1u << kProfAttn)) && (e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
         GemmParams go = gemm_base(E, d, qd, ncols);
         go.mode = kEpiAddF32;
@@ -349,7 +350,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             go.ss_out = E->norm_ss;
             go.ss_tiles = d / 128;
         }
-        if ((e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
+        if (!(E->skip_mask & (1u << kProfO)) && (e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);
         if (!fuse) {
             if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s,
@@ -368,7 +369,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             gu.norm_d = d;
             gu.norm_eps = c.eps;
         }
-        if ((e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
+        if (!(E->skip_mask & (1u << kProfGateUp)) && (e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfGateUp);
         GemmParams gd = gemm_base(E, d, c.F, ncols);
         gd.mode = kEpiAddF32;
@@ -378,7 +379,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             gd.ss_out = E->norm_ss;
             gd.ss_tiles = d / 128;
         }
-        if ((e = gemm_launch(Ly.tm_down, tm_act, gd, s, pdl)) != cudaSuccess) return e;
+        if (!(E->skip_mask & (1u << kProfDown)) && (e = gemm_launch(Ly.tm_down, tm_act, gd, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfDown);
         n += 6;
         if (fuse) {
@@ -900,6 +901,54 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
         if (ms_by_class) ms_by_class[k] = static_cast<float>(acc[k] / reps);
         if (launches_by_class) launches_by_class[k] = cnt[k];
     }
+    return DETGPU_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Timing experiment: capture a decode-step graph for ncols slots at context ctx with the kernel
+// classes in skip_mask left out (bit k = class k of detgpu_profile_decode_step), replay it `reps`
+// times and return the mean ms per step. Numerically meaningless when skip_mask != 0; never used
+// by generate().
+int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t skip_mask, uint32_t reps,
+                         float* ms_per_step) {
+    if (h == nullptr || h->e->toy) return fail(nullptr, DETGPU_EINVAL, "profile: transformer engine required");
+    Engine* E = h->e.get();
+    cudaSetDevice(E->device);
+    if (ncols == 0 || ncols > E->max_batch || ctx == 0 || ctx > E->max_context || reps == 0)
+        return fail(E, DETGPU_EINVAL, "profile: bad ncols/ctx/reps");
+    if (int rc = ensure_outputs(E, static_cast<int>(ncols), 2)) return rc;
+    std::vector<int> step(ncols, -1), pos(ncols, static_cast<int>(ctx) - 1), tok(ncols, 1), zero(ncols, 0);
+    std::vector<DevPolicy> dp(ncols, DevPolicy{DETGPU_GREEDY, 0, 0.0f, 1 << 30});
+    ENG_CUDA(cudaMemcpy(E->d_pol, dp.data(), sizeof(DevPolicy) * ncols, cudaMemcpyHostToDevice));
+    ENG_CUDA(cudaMemcpy(E->d_tok, tok.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    ENG_CUDA(cudaMemcpy(E->d_status, zero.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    // positions stay fixed across replays: the sampler is skipped via step = -1 unless asked for
+    ENG_CUDA(cudaMemcpy(E->d_pos, pos.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    ENG_CUDA(cudaMemcpy(E->d_step, step.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    E->skip_mask = skip_mask;
+    cudaGraph_t g;
+    ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
+    if (e == cudaSuccess) e = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, ncols <= 8);
+    cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
+    E->skip_mask = 0;
+    ENG_CUDA(e);
+    ENG_CUDA(e2);
+    cudaGraphExec_t ex;
+    ENG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    for (int i = 0; i < 3; ++i) ENG_CUDA(cudaGraphLaunch(ex, E->stream));
+    ENG_CUDA(cudaEventRecord(E->ev[0], E->stream));
+    for (uint32_t i = 0; i < reps; ++i) ENG_CUDA(cudaGraphLaunch(ex, E->stream));
+    ENG_CUDA(cudaEventRecord(E->ev[1], E->stream));
+    ENG_CUDA(cudaEventSynchronize(E->ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, E->ev[0], E->ev[1]);
+    cudaGraphExecDestroy(ex);
+    if (ms_per_step) *ms_per_step = ms / reps;
     return DETGPU_OK;
 }
 
