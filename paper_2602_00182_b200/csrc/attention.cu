@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     }
     const int nch = (ctx + CH - 1) / CH;
     __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    if (nch == 1) {
+    if (nch == 1 && !a.partials_only) {
         // single chunk: the combine weight is exp(0) == 1 exactly
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
@@ -184,17 +184,18 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         }
         return;
     }
-    float* wsb = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2);
-    float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 2);
+    float* wsb = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 4);
+    float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 4);
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
         const int ch = tid + j * kNT;
-        if (ch < CHAINS) ws[(ch / HD) * (HD + 2) + 2 + ch % HD] = acc[j];
+        if (ch < CHAINS) ws[(ch / HD) * (HD + 4) + 4 + ch % HD] = acc[j];
     }
     if (tid < G) {
-        ws[tid * (HD + 2)] = sM[tid];
-        ws[tid * (HD + 2) + 1] = sL[tid];
+        ws[tid * (HD + 4)] = sM[tid];
+        ws[tid * (HD + 4) + 1] = sL[tid];
     }
+    if (a.partials_only) return;   // the o-projection GEMM combines the chunks (gemm.cu attn_b_setup)
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -206,13 +207,13 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
+    const int64_t cstride = static_cast<int64_t>(G) * (HD + 4);
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
         const int ch = tid + j * kNT;
         if (ch >= CHAINS) continue;
         const int g = ch / HD, d = ch % HD;
-        const float* base = wsb + g * (HD + 2);
+        const float* base = wsb + g * (HD + 4);
         float M = -FLT_MAX;
         for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(base + cc * cstride));
         float L = 0.0f, O = 0.0f;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
             const float* w = base + cc * cstride;
             const float al = det_expf_shfl(__fsub_rn(__ldcg(w), M), tab);
             L = __fmaf_rn(__ldcg(w + 1), al, L);
-            O = __fmaf_rn(__ldcg(w + 2 + d), al, O);
+            O = __fmaf_rn(__ldcg(w + 4 + d), al, O);
         }
         outp[ch] = f2bf(__fdiv_rn(O, L));
     }
@@ -254,7 +255,7 @@ cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
 
 size_t attn_workspace_bytes(const AttnParams& a) {
     const int G = a.hq / a.hkv;
-    return sizeof(float) * static_cast<size_t>(a.ncols) * a.hkv * a.max_chunks * G * (a.hd + 2);
+    return sizeof(float) * static_cast<size_t>(a.ncols) * a.hkv * a.max_chunks * G * (a.hd + 4);
 }
 
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl) {

@@ -291,6 +291,13 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     // Decode with <= 8 columns: RMSNorm is fused into the consuming GEMMs (QKV, gate/up, lm_head),
     // which build their B operand from the f32 residual stream; bits are identical.
     const bool fuse = final_all && ncols <= 8;
+    // the o-projection combines the attention chunks itself when its K-segments fall on heads
+    bool fuse_attn = fuse && E->max_chunks <= 16;
+    {
+        const int S = gemm_ksplit(d, qd), nkb = qd / 64;
+        for (int sg = 0; sg <= S && fuse_attn; ++sg)
+            if (((sg * nkb / S) * 64) % c.hd != 0 || ((nkb * 64 / S) / c.hd) > 8) fuse_attn = false;
+    }
     e = launch_embed(E->embed, tok, E->x, fuse ? E->norm_ss : nullptr, E->layers[0].attn_norm, E->h, ncols, d, c.eps, s,
                      pdl);
     if (e != cudaSuccess) return e;
@@ -340,6 +347,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_pages = E->pages_per_slot;
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
+        a.partials_only = fuse_attn ? 1 : 0;   // the o-projection GEMM combines the chunks
         if (!(E->skip_mask & (1u << kProfAttn)) && (e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
         GemmParams go = gemm_base(E, d, qd, ncols);
@@ -349,6 +357,15 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         if (fuse) {
             go.ss_out = E->norm_ss;
             go.ss_tiles = d / 128;
+        }
+        if (fuse_attn) {
+            go.attn_ws = E->attn_ws;
+            go.attn_pos = pos;
+            go.attn_hkv = c.hkv;
+            go.attn_G = c.hq / c.hkv;
+            go.attn_hd = c.hd;
+            go.attn_max_chunks = E->max_chunks;
+            go.attn_chunk = kAttnChunk;
         }
         if (!(E->skip_mask & (1u << kProfO)) && (e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);

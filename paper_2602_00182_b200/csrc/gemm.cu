@@ -8,6 +8,8 @@
 // Reference counterpart: det_matvec (reference proj/src/detcore.cpp:165-185), one output element
 // per weight row; here the reduction order over K is fixed by the k-block loop below and never
 // split across CTAs.
+#include <cfloat>
+
 #include "gemm.cuh"
 #include "detmath.cuh"
 #include "ptx.cuh"
@@ -21,6 +23,7 @@ constexpr int BK = 64;
 constexpr int SUB_N = 64;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int B_BYTES = SUB_N * BK * 2;     // 8 KB
+constexpr int kMaxBc = 35;                  // k-blocks of a fused B buffer
 
 template <int NSUB>
 struct Cfg {
@@ -30,7 +33,9 @@ struct Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + NSUB * B_BYTES;
     static constexpr int BUDGET = NSUB <= 2 ? 96 * 1024 : 192 * 1024;
     static constexpr int STAGES = BUDGET / STAGE_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    // one-column-group decode: 10 KB more so the fused B buffer (the B ring + this) holds 35 k-blocks
+    static constexpr int BC_EXTRA = NSUB == 1 ? 10 * 1024 : 0;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + BC_EXTRA + 1024 /*align*/ + 640 /*barriers*/;
     static constexpr int MIN_CTAS = NSUB <= 2 ? 2 : 1;
     static constexpr uint32_t TMEM = NSUB * SUB_N;   // f32 accumulator columns (power of two)
 };
@@ -154,33 +159,35 @@ __device__ __forceinline__ float norm_sumsq(const float* row, int d, int lane) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// Epilogue warps as the B-operand producer: rstd per column, then for every k-block of the segment
-// bf16((x * rstd) * gamma) written straight into the stage's 128B-swizzled K-major tile (row = col,
-// 16-byte chunk j of the 128-byte row stored at chunk j ^ (row % 8)). Rows >= ncols are left as
-// they are: MMA columns are independent, and those columns are never stored.
-template <int STAGES>
-__device__ void norm_b_producer(const GemmParams& p, uint8_t* sB, uint64_t* full, uint64_t* empty, int kb0, int nkb,
-                                int col0, int ncols, int ew, int lane) {
+// Fused B operand (decode, <= 8 columns). The epilogue warps, idle until the accumulator is
+// ready, build the B tiles of the CTA's whole K-segment once, straight into a compact shared
+// buffer: k-block i occupies 1 KB at bc + i*1024 holding rows 0..7 in the 128B-swizzled K-major
+// layout (16-byte chunk j of row r stored at chunk j ^ r). The MMA's 64-row descriptor at
+// bc + i*1024 also covers rows 8..63, which are the following k-blocks' bytes: those are the
+// padding columns of the N=64 instruction and are never stored (columns are independent).
+// Values (bits identical to the unfused kernels):
+//   norm: bf16((x * rstd) * gamma), rstd from the producer's per-tile sums of squares
+//   attn: bf16(O / L) of the chunk partials combined in chunk order (attention.cu)
+__device__ __forceinline__ void put_b(uint8_t* bc, int i, int c, int kq, float v0, float v1, float v2, float v3) {
+    uint2 packed;
+    packed.x = static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(v0))) |
+               (static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(v1))) << 16);
+    packed.y = static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(v2))) |
+               (static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(v3))) << 16);
+    const int chunk = (kq >> 3) ^ (c & 7);
+    *reinterpret_cast<uint2*>(bc + i * 1024 + c * 128 + chunk * 16 + (kq & 7) * 2) = packed;
+}
+
+// every producer thread: make its k-block writes visible to the tensor core, then arrive
+__device__ __forceinline__ void release_b(uint64_t* bready, int i) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&bready[i]);
+}
+
+__device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready, int kb0, int nkb, int col0,
+                             int ncols, int ew, int lane) {
     __shared__ float s_rstd[8];
-    const int d = p.norm_d;
-    const int t = ew * 32 + lane;
-    const int c = t >> 4, kq = (t & 15) * 4;   // column, first of 4 consecutive k in the block
-    const bool active = c < ncols;
-    const float* xrow = p.norm_x + static_cast<int64_t>(col0 + (active ? c : 0)) * d + kq;
-    const __nv_bfloat16* grow = p.norm_gamma + kq;
-    // software pipeline: the x / gamma values of the next PF k-blocks are in flight in registers
-    // (issued before the rstd reduction so both latencies overlap)
-    constexpr int PF = 8;
-    float4 xr[PF];
-    uint2 gr[PF];
-#pragma unroll
-    for (int j = 0; j < PF; ++j) {
-        if (active && j < nkb) {
-            xr[j] = *reinterpret_cast<const float4*>(xrow + (kb0 + j) * BK);
-            gr[j] = *reinterpret_cast<const uint2*>(grow + (kb0 + j) * BK);
-        }
-    }
-    const int ntiles = d / 128;
+    const int d = p.norm_d, ntiles = d / 128;
     for (int cc = ew; cc < ncols; cc += 4) {
         // the producer of x left one partial per 128-row tile; their tree is the tree over d
         const float part = lane < ntiles ? p.norm_ss[static_cast<int64_t>(col0 + cc) * ntiles + lane] : kNegZero;
@@ -191,42 +198,82 @@ __device__ void norm_b_producer(const GemmParams& p, uint8_t* sB, uint64_t* full
         }
     }
     epi_bar();
-    const float rstd = active ? s_rstd[c] : 0.0f;
-    for (int i0 = 0; i0 < nkb; i0 += PF) {
-#pragma unroll
-        for (int j = 0; j < PF; ++j) {
-            const int i = i0 + j;
-            if (i >= nkb) break;   // uniform across the 128 producer threads
-            const int s = i % STAGES;
-            uint2 packed = make_uint2(0u, 0u);
-            if (active) {
-                const float4 xv = xr[j];
-                const uint2 gv = gr[j];
-                if (i + PF < nkb) {
-                    xr[j] = *reinterpret_cast<const float4*>(xrow + (kb0 + i + PF) * BK);
-                    gr[j] = *reinterpret_cast<const uint2*>(grow + (kb0 + i + PF) * BK);
-                }
-                const float g0 = __uint_as_float(gv.x << 16), g1 = __uint_as_float(gv.x & 0xffff0000u);
-                const float g2 = __uint_as_float(gv.y << 16), g3 = __uint_as_float(gv.y & 0xffff0000u);
-                const __nv_bfloat16 h0 = f2bf(__fmul_rn(__fmul_rn(xv.x, rstd), g0));
-                const __nv_bfloat16 h1 = f2bf(__fmul_rn(__fmul_rn(xv.y, rstd), g1));
-                const __nv_bfloat16 h2 = f2bf(__fmul_rn(__fmul_rn(xv.z, rstd), g2));
-                const __nv_bfloat16 h3 = f2bf(__fmul_rn(__fmul_rn(xv.w, rstd), g3));
-                packed.x = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
-                           (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
-                packed.y = static_cast<uint32_t>(__bfloat16_as_ushort(h2)) |
-                           (static_cast<uint32_t>(__bfloat16_as_ushort(h3)) << 16);
-            }
-            if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-            if (active) {
-                const int chunk = (kq >> 3) ^ (c & 7);
-                *reinterpret_cast<uint2*>(sB + s * B_BYTES + c * 128 + chunk * 16 + (kq & 7) * 2) = packed;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-            epi_bar();
-            if (t == 0) mbar_arrive(&full[s]);
-        }
+    // quad q = (column, k-block, 4 consecutive k): all of the segment's loads are issued at once
+    const int t = ew * 32 + lane;
+    const int per_col = nkb * 16, total = ncols * per_col;
+#pragma unroll 4
+    for (int q = t; q < total; q += 128) {
+        const int c = q / per_col, rem = q % per_col, i = rem >> 4, kq = (rem & 15) * 4;
+        const float rstd = s_rstd[c];
+        const int k = (kb0 + i) * BK + kq;
+        const float4 xv = *reinterpret_cast<const float4*>(p.norm_x + static_cast<int64_t>(col0 + c) * d + k);
+        const uint2 gv = *reinterpret_cast<const uint2*>(p.norm_gamma + k);
+        put_b(bc, i, c, kq, __fmul_rn(__fmul_rn(xv.x, rstd), __uint_as_float(gv.x << 16)),
+              __fmul_rn(__fmul_rn(xv.y, rstd), __uint_as_float(gv.x & 0xffff0000u)),
+              __fmul_rn(__fmul_rn(xv.z, rstd), __uint_as_float(gv.y << 16)),
+              __fmul_rn(__fmul_rn(xv.w, rstd), __uint_as_float(gv.y & 0xffff0000u)));
     }
+    for (int i = 0; i < nkb; ++i) release_b(bready, i);
+}
+
+// O-projection input from attention chunk partials ws[col][kvh][chunk][g][4 + hd] = (m, l, -, -, o[hd]).
+__device__ void attn_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready, int kb0, int nkb, int col0,
+                             int ncols, int ew, int lane, ExpTab tab) {
+    constexpr int kMaxH = 8, kMaxC = 16;
+    __shared__ float s_al[8][kMaxH][kMaxC];   // combine weights a_c per (column, head)
+    __shared__ float s_L[8][kMaxH];
+    const int hd = p.attn_hd, G = p.attn_G, hkv = p.attn_hkv, mc = p.attn_max_chunks;
+    const int h0 = kb0 * BK / hd;                            // first head of this K-segment
+    const int nh = (nkb * BK + hd - 1) / hd;
+    auto wsp = [&](int col, int h, int ch) {
+        return p.attn_ws + ((static_cast<int64_t>(col0 + col) * hkv + h / G) * mc + ch) * G * (hd + 4) +
+               (h % G) * (hd + 4);
+    };
+    // per (column, head): M = max_c m_c, a_c = exp(m_c - M), L = fma chain of l_c a_c (chunk order)
+    for (int q = ew; q < ncols * nh; q += 4) {
+        const int cc = q / nh, hl = q % nh, h = h0 + hl;
+        const int pos = p.attn_pos[col0 + cc];
+        const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
+        // lane ch holds chunk ch's (m, l); the chain runs on shuffled registers, in chunk order
+        const float m = lane < nch ? __ldcg(wsp(cc, h, lane)) : -FLT_MAX;
+        const float l = lane < nch ? __ldcg(wsp(cc, h, lane) + 1) : 0.0f;
+        const float M = warp_max(m);
+        const float al = det_expf_shfl(lane < nch ? __fsub_rn(m, M) : 0.0f, tab);   // all lanes
+        if (lane < nch) s_al[cc][hl][lane] = al;
+        float L = 0.0f;
+        for (int ch = 0; ch < nch; ++ch)
+            L = __fmaf_rn(__shfl_sync(0xffffffffu, l, ch), __shfl_sync(0xffffffffu, al, ch), L);
+        if (lane == 0) s_L[cc][hl] = L;
+    }
+    epi_bar();
+    const int t = ew * 32 + lane;
+    const int per_col = nkb * 16, total = ncols * per_col;
+#pragma unroll 2
+    for (int q = t; q < total; q += 128) {
+        const int c = q / per_col, rem = q % per_col, i = rem >> 4, kq = (rem & 15) * 4;
+        const int pos = p.attn_pos[col0 + c];
+        const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
+        const int k = (kb0 + i) * BK + kq;   // input feature = head * hd + d
+        const int h = k / hd, hl = h - h0, dd = k % hd;
+        float4 ov[kMaxC];
+#pragma unroll
+        for (int ch = 0; ch < kMaxC; ++ch)   // all loads in flight before the chain
+            if (ch < nch) ov[ch] = __ldcg(reinterpret_cast<const float4*>(wsp(c, h, ch) + 4 + dd));
+        float O0 = 0.0f, O1 = 0.0f, O2 = 0.0f, O3 = 0.0f;
+#pragma unroll
+        for (int ch = 0; ch < kMaxC; ++ch) {
+            if (ch < nch) {
+                const float a = s_al[c][hl][ch];
+                O0 = __fmaf_rn(ov[ch].x, a, O0);
+                O1 = __fmaf_rn(ov[ch].y, a, O1);
+                O2 = __fmaf_rn(ov[ch].z, a, O2);
+                O3 = __fmaf_rn(ov[ch].w, a, O3);
+            }
+        }
+        const float L = s_L[c][hl];
+        put_b(bc, i, c, kq, __fdiv_rn(O0, L), __fdiv_rn(O1, L), __fdiv_rn(O2, L), __fdiv_rn(O3, L));
+    }
+    for (int i = 0; i < nkb; ++i) release_b(bready, i);
 }
 
 // Grid (S, n_out/128, column groups), cluster (S,1,1): the S CTAs of a cluster own the same 128
@@ -244,10 +291,11 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NSUB * B_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NSUB * B_BYTES + C::BC_EXTRA);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* bready = tfull + 1;        // [kMaxBc] fused B: k-block i ready (128 producer arrivals)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bready + kMaxBc);
 
     __shared__ float s_red[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -263,16 +311,19 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     // Fused RMSNorm (decode, <= 8 columns): the B operand is produced in shared memory by the
     // epilogue warps from the f32 residual stream instead of being loaded by TMA from a separately
     // normalised bf16 copy; bits are identical to rmsnorm_kernel + TMA.
-    const bool fused = p.norm_x != nullptr;
+    const int bmode = p.norm_x != nullptr ? 1 : (p.attn_ws != nullptr ? 2 : 0);
+    const bool fused = bmode != 0;
+    uint8_t* bc = sB;   // fused B buffer: 1 KB per k-block (see norm_b_setup)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmX);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], fused ? 2 : 1);   // fused norm: TMA (A) + software producer (B)
+            mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
+        for (int i = 0; i < kMaxBc; ++i) mbar_init(&bready[i], 128);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tslot, C::TMEM);
@@ -324,10 +375,11 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             constexpr uint32_t idesc = umma_idesc_bf16(BM, SUB_N);
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % STAGES;
+                if (fused) mbar_wait(&bready[i], 0);
                 mbar_wait(&full[s], (i / STAGES) & 1);
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-                const uint32_t b_base = smem_u32(sB + s * NSUB * B_BYTES);
+                const uint32_t b_base = fused ? smem_u32(bc + i * 1024) : smem_u32(sB + s * NSUB * B_BYTES);
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) {
                     const uint64_t adesc = umma_desc_k128(a_base + k * 32);
@@ -344,7 +396,10 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         const int ew = warp - 4;       // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
         const int rl = ew * 32 + lane;
         const ExpTab tab = exp_tab_lane();
-        if (fused) norm_b_producer<STAGES>(p, sB, full, empty, kb0, nkb, col0, ncols, ew, lane);
+        if (fused) {
+            if (bmode == 1) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
+            else attn_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane, tab);
+        }
         mbar_wait(tfull, 0);
         tc_fence_after();
         float* P = reinterpret_cast<float*>(smem);   // partial tile [col][128] (stages are idle now)
@@ -492,6 +547,14 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     GemmParams p = p_in;
     if (p.ksplit <= 0) p.ksplit = gemm_ksplit(p.n_out, p.k);
     if (p.ksplit > 8 || p.ksplit > p.k / BK) return cudaErrorInvalidValue;
+    const int seg_kb = (p.k / BK + p.ksplit - 1) / p.ksplit;
+    if ((p.norm_x != nullptr || p.attn_ws != nullptr) && (p.ncols > 8 || seg_kb > 35)) return cudaErrorInvalidValue;
+    if (p.attn_ws != nullptr) {
+        if (p.attn_max_chunks > 16 || p.attn_hd % 64 != 0 || (seg_kb * BK) / p.attn_hd > 8 || p.norm_x != nullptr)
+            return cudaErrorInvalidValue;
+        for (int sg = 0; sg <= p.ksplit; ++sg)   // every K-segment boundary must fall on a head boundary
+            if (((sg * (p.k / BK) / p.ksplit) * BK) % p.attn_hd != 0) return cudaErrorInvalidValue;
+    }
     if (p.norm_x != nullptr && (p.ncols > 8 || p.norm_ss == nullptr || p.k != p.norm_d || (p.norm_d & (p.norm_d - 1)) != 0 ||
                                 p.norm_d < 256 || p.norm_d > 4096))
         return cudaErrorInvalidValue;

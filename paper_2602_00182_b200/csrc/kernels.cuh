@@ -49,6 +49,7 @@ struct AttnParams {
     int* tickets;                  // [ncols][hkv], zero-initialised; reset by the combining CTA
     int ncols, hq, hkv, hd, page, max_pages, max_chunks;
     int decode;                    // 1: every column's positions < pos were written by earlier launches
+    int partials_only;             // 1: write every chunk's (m, l, o) and stop; the o-GEMM combines
 };
 size_t attn_workspace_bytes(const AttnParams& a);
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);
