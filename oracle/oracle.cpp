@@ -712,9 +712,9 @@ static void rmsnorm(const float* x, const uint16_t* gamma, int d, float eps, uin
     for (int i = 0; i < d; ++i) out[i] = bf16_rne((x[i] * rstd) * bf2f(gamma[i]));
 }
 
-constexpr int kChunk = 128;
+constexpr int kChunk = 64;
 // Attention for one query head against positions [0, ctx) of a contiguous cache k[p][hd], v[p][hd]
-// (DESIGN.md §3.5): fixed 128-position chunks, tree-summed dot products and chunk sums, fma chains
+// (DESIGN.md §3.5): fixed 64-position chunks, tree-summed dot products and chunk sums, fma chains
 // for the weighted values, chunk-order combine.
 static void attention_head(const uint16_t* q, const uint16_t* const* kp, const uint16_t* const* vp, int ctx, int hd,
                            float scale, uint16_t* out) {

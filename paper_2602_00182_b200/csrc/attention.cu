@@ -7,7 +7,7 @@
 // and the chunks are combined in chunk order by whichever CTA of the (column, kv head) finishes
 // last (a ticket elects the combiner; the combination itself is order-fixed):
 //   a_c = exp(m_c - max m) ; out_d = bf16( (sum_c fma o_cd a_c) / (sum_c fma l_c a_c) )
-// Chunk boundaries are positions 128c, so split-KV parallelism never changes a bit and prefill
+// Chunk boundaries are positions 64c, so split-KV parallelism never changes a bit and prefill
 // queries see exactly the same arithmetic as decode steps.
 #include <cfloat>
 
@@ -131,23 +131,24 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     // chunk softmax pieces: warp g owns head g (4 positions per lane)
     const ExpTab tab = exp_tab_lane();
     for (int g = warp; g < G; g += kNW) {
-        float sv[4], e[4];
+        constexpr int PPL = CH / 32;   // positions per lane
+        float sv[PPL], e[PPL];
         float m = -FLT_MAX;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int p = lane * 4 + j;
+        for (int j = 0; j < PPL; ++j) {
+            const int p = lane * PPL + j;
             sv[j] = p < n ? sS[g * CH + p] : 0.0f;
             if (p < n) m = fmaxf(m, sv[j]);
         }
         m = warp_max(m);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int p = lane * 4 + j;
+        for (int j = 0; j < PPL; ++j) {
+            const int p = lane * PPL + j;
             const float ev = det_expf_shfl(p < n ? __fsub_rn(sv[j], m) : 0.0f, tab);
             e[j] = p < n ? ev : kNegZero;
             sS[g * CH + p] = e[j];
         }
-        float l = local_tree_sum<4>(e);
+        float l = local_tree_sum<PPL>(e);
         l = warp_tree_sum(l);
         if (lane == 0) {
             sM[g] = m;

@@ -10,7 +10,7 @@ namespace detgpu {
 
 // Attention KV chunk: positions [c*kAttnChunk, (c+1)*kAttnChunk) form one online-softmax chunk,
 // combined in chunk order. Part of the numeric definition; never batch-dependent.
-constexpr int kAttnChunk = 128;
+constexpr int kAttnChunk = 64;
 
 // ---- RMSNorm (optionally with the embedding gather fused in) ----
 // x_in [rows][d] f32 (row = col_index ? col_index[col] : col); when embed != nullptr the input row
