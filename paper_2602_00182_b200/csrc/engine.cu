@@ -264,6 +264,7 @@ void mark(Engine* E, int cls) {
 GemmParams gemm_base(const Engine* E, int n_out, int k, int ncols) {
     GemmParams p{};
     p.w_tiled = 1;   // engine weights are stored pre-tiled
+    p.mma_wide = 1;  // one N = 64*sub-tiles MMA per K step: column bits identical (tools/wide_mma_check.py)
 
     p.n_out = n_out;
     p.k = k;

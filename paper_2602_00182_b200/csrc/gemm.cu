@@ -373,6 +373,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_bf16(BM, SUB_N);
+            const bool wide = p.mma_wide && !fused && nb > 1;
+            const uint32_t idesc_wide = umma_idesc_bf16(BM, nb * SUB_N);
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % STAGES;
                 if (fused) mbar_wait(&bready[i], 0);
@@ -380,12 +382,20 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA + s * A_BYTES);
                 const uint32_t b_base = fused ? smem_u32(bc + i * 1024) : smem_u32(sB + s * NSUB * B_BYTES);
+                if (wide) {
+                    // all live sub-tiles as one N = nb*64 instruction (A read once from smem)
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t adesc = umma_desc_k128(a_base + k * 32);
-                    for (int j = 0; j < nb; ++j) {
-                        const uint64_t bdesc = umma_desc_k128(b_base + j * B_BYTES + k * 32);
-                        tc_mma_bf16(tbase + j * SUB_N, adesc, bdesc, idesc, (i | k) != 0 ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc_mma_bf16(tbase, umma_desc_k128(a_base + k * 32), umma_desc_k128(b_base + k * 32), idesc_wide,
+                                    (i | k) != 0 ? 1u : 0u);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t adesc = umma_desc_k128(a_base + k * 32);
+                        for (int j = 0; j < nb; ++j) {
+                            const uint64_t bdesc = umma_desc_k128(b_base + j * B_BYTES + k * 32);
+                            tc_mma_bf16(tbase + j * SUB_N, adesc, bdesc, idesc, (i | k) != 0 ? 1u : 0u);
+                        }
                     }
                 }
                 tc_commit(&empty[s]);   // frees the smem stage once these MMAs retire

@@ -29,6 +29,7 @@ struct GemmParams {
     int mode;
     int ksplit;  // 0: gemm_ksplit(n_out, k) (the engine's numeric definition); >0: explicit (test hooks)
     int w_tiled; // weights pre-tiled [n_out/128][K/64][128][64] (engine) or plain row-major
+    int mma_wide;// 1: one N = nb*64 MMA per K=16 step instead of nb N=64 ones (same column bits)
     // kEpiStoreF32 / kEpiAddF32
     float* out;
     int64_t ld_out;            // per-column stride of `out` (elements)

@@ -92,3 +92,21 @@ def test_repeat_bitwise():
     first = _gemm(W, X)
     for _ in range(20):
         assert torch.equal(_gemm(W, X).view(torch.int32), first.view(torch.int32))
+
+
+def test_wide_mma_form_is_bit_identical():
+    """One N = nb*64 tcgen05.mma per K step (the engine's form) gives the same column bits as nb
+    separate N = 64 instructions."""
+    import torch
+    from paper_2602_00182_b200._lib import check, lib
+
+    g = torch.Generator().manual_seed(5)
+    for n_out, K, ncols in [(256, 512, 256), (512, 4096, 200), (384, 256, 70)]:
+        W = _rand_bf16((n_out, K), g, 0.05)
+        X = _rand_bf16((ncols, K), g)
+        Y1 = torch.empty(ncols, n_out, device="cuda")
+        Y2 = torch.empty(ncols, n_out, device="cuda")
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y1.data_ptr(), n_out, K, ncols, n_out, 0, None))
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y2.data_ptr(), n_out, K, ncols, n_out, -1, None))
+        torch.cuda.synchronize()
+        assert torch.equal(Y1.view(torch.int32), Y2.view(torch.int32))
