@@ -124,6 +124,21 @@ void* detgpu_stream(const detgpu_engine* h);
 int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t reps,
                                float* ms_by_class, uint32_t* launches_by_class);
 
+/* Scheduling knobs that never change a result bit (timing experiments / deployment tuning):
+ *   "l2pf_mask"   which decode kernels warm the next kernel's weights into L2 (bit 0 attention->o,
+ *                 1 o->gate/up, 2 gate/up->down, 3 down->next QKV, 4 QKV->o)
+ *   "l2pf_cap_mb" cap on the bytes one kernel warms
+ *   "pdl"         programmatic dependent launch on (1) / off (0)
+ *   "attn_fuse"   decode: combine attention chunks in the o-projection GEMM (1) or in the
+ *                 attention kernel's cluster (0, default)
+ *   "trace"       > 0: record a per-CTA timeline of the decode kernels (capacity in records), 0: off
+ * Cached decode graphs are dropped. Returns DETGPU_EINVAL for an unknown name. */
+int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value);
+
+/* Copy up to max_records timeline records (32 bytes each: u32 tag = class << 24 | CTA, u32 sm,
+ * u64 t_start, t_wait_released, t_end in globaltimer ns) and reset the buffer. */
+int detgpu_trace_read(detgpu_engine* h, void* out, uint32_t max_records, uint32_t* n_records);
+
 /* Timing experiment: mean ms of a captured decode-step graph with the kernel classes of skip_mask
  * left out (results meaningless when skip_mask != 0). Measurement hook only. */
 int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t skip_mask, uint32_t reps,

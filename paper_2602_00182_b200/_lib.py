@@ -8,7 +8,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libdetgpu.so"
+import os
+
+# DETGPU_LIB selects an experiment build (build.py --variant) for A/B timing; default: the product.
+LIB_PATH = Path(os.environ.get("DETGPU_LIB") or Path(__file__).resolve().parent / "libdetgpu.so")
 
 DETGPU_OK = 0
 DETGPU_EINVAL = 1
@@ -58,6 +61,8 @@ def _load() -> C.CDLL:
         "detgpu_stream": (vp, [vp]),
         "detgpu_profile_decode_step": (i32, [vp, u32, u32, u32, C.POINTER(C.c_float), C.POINTER(u32)]),
         "detgpu_profile_graph": (i32, [vp, u32, u32, u32, u32, C.POINTER(C.c_float)]),
+        "detgpu_set_option": (i32, [vp, C.c_char_p, C.c_int64]),
+        "detgpu_trace_read": (i32, [vp, vp, u32, C.POINTER(u32)]),
         "detgpu_sha256": (None, [vp, sz, vp]),
         "detgpu_canonical_size": (sz, [u32, u32]),
         "detgpu_encode_canonical": (None, [vp, u32, vp, u32, vp]),

@@ -39,32 +39,35 @@ def _stale(out: Path, inputs: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in inputs)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> Path:
+def build_lib(force: bool = False, verbose: bool = False, variant: str = "", defines: tuple = ()) -> Path:
+    """`variant` + `defines` build an alternative libdetgpu_<variant>.so (A/B timing experiments,
+    loaded with DETGPU_LIB=...); the default build is the product."""
+    lib_out = LIB if not variant else PKG / f"libdetgpu_{variant}.so"
     srcs = _sources()
     deps = srcs + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = PKG / "build"
+    if not force and not _stale(lib_out, deps):
+        return lib_out
+    objdir = PKG / ("build" if not variant else f"build_{variant}")
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in srcs:
         obj = objdir / (src.name + ".o")
         hdrs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
         if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src.name}")
         objs.append(obj)
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB), *map(str, objs),
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib_out), *map(str, objs),
            "-Xcompiler", "-fPIC", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link of libdetgpu.so failed")
-    return LIB
+    return lib_out
 
 
 def build_oracle(force: bool = False) -> None:
@@ -85,6 +88,10 @@ def build_oracle(force: bool = False) -> None:
 
 if __name__ == "__main__":
     force = "--force" in sys.argv
+    if "--variant" in sys.argv:   # --variant NAME DEFINE [DEFINE ...]
+        i = sys.argv.index("--variant")
+        print(build_lib(force=force, variant=sys.argv[i + 1], defines=tuple(sys.argv[i + 2:])))
+        sys.exit(0)
     build_lib(force=force, verbose="-v" in sys.argv)
     if "--lib-only" not in sys.argv:
         build_oracle(force=force)

@@ -20,9 +20,14 @@ namespace detgpu {
 namespace {
 
 constexpr int kNT = 256;           // threads per CTA
+constexpr int kMaxClusterChunks = 16;   // cluster mode: chunks of one (column, kv head) per cluster
 constexpr int kNW = kNT / 32;
 
-template <int HD, int G>
+// CL (cluster mode): the chunk CTAs of one (column, kv head) form a cluster; chunk 0 (the leader)
+// receives every other chunk's (m, l, o) by st.async into its K/V buffer once it has finished with
+// it, combines them in chunk order and writes the output: no workspace, no ticket, no grid-wide
+// round trip. Same arithmetic as the ticket combine below.
+template <int HD, int G, bool CL>
 __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, float scale) {
     constexpr int CH = kAttnChunk;
     constexpr int E = HD / 32;                       // q/k elements per lane in a dot product
@@ -35,8 +40,37 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __shared__ float sS[G * CH];
     __shared__ float sM[G], sL[G];
     __shared__ int s_last;
+    __shared__ uint64_t s_bar[2];   // CL: [0] leader: partials landed, [1] pusher: leader's K/V buffer free
+    __shared__ float s_al[CL ? G : 1][CL ? kMaxClusterChunks : 1], s_mx[G];
 
     const int c = blockIdx.x, kvh = blockIdx.y, col = blockIdx.z;
+    struct TraceAtExit {   // records the CTA's timeline on every return path (instrumentation only)
+        const AttnParams& a;
+        uint64_t m[kTraceMarks];
+        __device__ void mark(int i) {
+            if (a.trace != nullptr) m[i] = globaltimer_ns();
+        }
+        __device__ ~TraceAtExit() {
+            if (threadIdx.x == 0 && a.trace != nullptr)
+                trace_record(a.trace, (a.trace_tag << 24) | (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)),
+                             m);
+        }
+    } tr{a, {a.trace != nullptr ? globaltimer_ns() : 0}};
+    if (threadIdx.x == 0)
+        l2_prefetch_slice(a.l2pf, a.l2pf_bytes, c + gridDim.x * (kvh + gridDim.y * col),
+                          gridDim.x * gridDim.y * gridDim.z);
+    if constexpr (CL) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        cluster_arrive();   // every CTA of the cluster, active or not, arrives once and waits once
+    }
+    auto leave = [&]() {
+        if constexpr (CL) cluster_wait();
+    };
     // Decode: positions < pos were written by earlier steps and col_pos by the previous step's
     // sampler; every kernel waits for its predecessor before triggering (gemm.cu), so both are
     // complete when this kernel starts and the chunk's K/V can stream while the QKV GEMM (the
@@ -45,12 +79,19 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     if (!a.decode) {
         pdl_wait();
         pdl_trigger();
+        tr.mark(1);
     }
     const int pos = a.col_pos[col];
-    if (pos < 0) return;
+    if (pos < 0) {
+        leave();
+        return;
+    }
     const int ctx = pos + 1;
     const int p0 = c * CH;
-    if (p0 >= ctx) return;
+    if (p0 >= ctx) {
+        leave();
+        return;
+    }
     const int n = min(CH, ctx - p0);
     const int slot = a.col_req[col];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -72,6 +113,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         load_rows(0, pos - p0 < n ? pos - p0 : n);   // history rows, before the wait
         pdl_wait();
         pdl_trigger();
+        tr.mark(1);
         if (pos - p0 < n) load_rows(pos - p0, n);     // the row the QKV GEMM just appended
     } else {
         load_rows(0, n);
@@ -81,6 +123,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     for (int i = tid; i < G * HD; i += kNT) sQ[i] = bf2f(qsrc[i]);
     cp_async_wait_all();
     __syncthreads();
+    tr.mark(2);   // K/V chunk and q in shared memory
 
     // scores: each warp takes two positions per step; 2G butterflies interleaved
     float q[G][E];
@@ -127,6 +170,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         }
     }
     __syncthreads();
+    tr.mark(3);   // scores
 
     // chunk softmax pieces: warp g owns head g (4 positions per lane)
     const ExpTab tab = exp_tab_lane();
@@ -156,6 +200,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         }
     }
     __syncthreads();
+    tr.mark(4);   // softmax
 
     // o: chain (g, d) = fma over positions in order
     float acc[CPT];
@@ -173,8 +218,69 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
             }
         }
     }
+    tr.mark(5);   // PV chains
     const int nch = (ctx + CH - 1) / CH;
     __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    if constexpr (CL) {
+        if (nch > 1) {
+            constexpr int BLK = G * (HD + 2);   // one pushed partial: m[G], l[G], o[G][HD]
+            float* recv = reinterpret_cast<float*>(attn_dsm);
+            if (c == 0) {
+                __syncthreads();   // the leader's own K/V reads are complete
+                if (tid == 0) mbar_arrive_expect_tx(&s_bar[0], static_cast<uint32_t>((nch - 1) * BLK * 4));
+                cluster_wait();
+                if (tid >= 1 && tid < nch) mbar_arrive_remote(mapa_shared(smem_u32(&s_bar[1]), tid));
+                if (tid < G) {
+                    float M = sM[tid];   // chunk order: fmaxf chain from -FLT_MAX (see the ticket combine)
+                    M = fmaxf(-FLT_MAX, M);
+                    mbar_wait(&s_bar[0], 0);
+                    for (int cc = 1; cc < nch; ++cc) M = fmaxf(M, recv[(cc - 1) * BLK + tid]);
+                    s_mx[tid] = M;
+                } else {
+                    mbar_wait(&s_bar[0], 0);
+                }
+                __syncthreads();
+                const ExpTab tab2 = exp_tab_lane();
+                if (tid < ((G * kMaxClusterChunks + 31) & ~31)) {   // warp-uniform: det_expf_shfl needs all lanes
+                    const int g = tid / kMaxClusterChunks, cc = tid % kMaxClusterChunks;
+                    const bool ok = g < G && cc < nch;
+                    const float m = !ok ? 0.0f : cc == 0 ? sM[g] : recv[(cc - 1) * BLK + g];
+                    const float al = det_expf_shfl(ok ? __fsub_rn(m, s_mx[g < G ? g : 0]) : 0.0f, tab2);
+                    if (ok) s_al[g][cc] = al;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    const int ch = tid + j * kNT;
+                    if (ch >= CHAINS) continue;
+                    const int g = ch / HD, d = ch % HD;
+                    float L = __fmaf_rn(sL[g], s_al[g][0], 0.0f), O = __fmaf_rn(acc[j], s_al[g][0], 0.0f);
+                    for (int cc = 1; cc < nch; ++cc) {
+                        const float* w = recv + (cc - 1) * BLK;
+                        L = __fmaf_rn(w[G + g], s_al[g][cc], L);
+                        O = __fmaf_rn(w[2 * G + g * HD + d], s_al[g][cc], O);
+                    }
+                    outp[ch] = f2bf(__fdiv_rn(O, L));
+                }
+            } else {
+                cluster_wait();
+                mbar_wait(&s_bar[1], 0);   // the leader no longer reads its K/V buffer
+                const uint32_t rb = mapa_shared(smem_u32(recv) + 4u * static_cast<uint32_t>((c - 1) * BLK), 0);
+                const uint32_t rbar = mapa_shared(smem_u32(&s_bar[0]), 0);
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    const int ch = tid + j * kNT;
+                    if (ch < CHAINS) st_async_f32(rb + 4u * (2 * G + ch), acc[j], rbar);
+                }
+                if (tid < G) {
+                    st_async_f32(rb + 4u * tid, sM[tid], rbar);
+                    st_async_f32(rb + 4u * (G + tid), sL[tid], rbar);
+                }
+            }
+            return;
+        }
+        leave();
+    }
     if (nch == 1 && !a.partials_only) {
         // single chunk: the combine weight is exp(0) == 1 exactly
 #pragma unroll
@@ -228,13 +334,15 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     }
 }
 
-template <int HD, int G>
-cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
+template <int HD, int G, bool CL>
+cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
     constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(dsm));
+        cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+        if (e == cudaSuccess && CL)
+            e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -243,13 +351,26 @@ cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
     cfg.blockDim = dim3(kNT);
     cfg.dynamicSmemBytes = dsm;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CL ? a.max_chunks : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(HD)));
-    return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G>, a, scale);
+    return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G, CL>, a, scale);
+}
+
+// Cluster combine when the chunks of a (column, kv head) fit one cluster and the pushed partials
+// fit the leader's K/V buffer; the workspace/ticket combine otherwise.
+template <int HD, int G>
+cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    const bool cl = !a.partials_only && a.max_chunks <= kMaxClusterChunks &&
+                    static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 <= 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
+    return cl ? launch_hgc<HD, G, true>(a, stream, pdl) : launch_hgc<HD, G, false>(a, stream, pdl);
 }
 
 }  // namespace

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -98,6 +99,15 @@ struct Engine {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<std::pair<cudaEvent_t, int>>* prof = nullptr;
     unsigned skip_mask = 0;   // timing experiments only (detgpu_profile_graph): kernel classes left out
+    // Decode: which kernels warm the NEXT kernel's weights into L2 at their start (bit 0: attention ->
+    // o, 1: o -> gate/up, 2: gate/up -> down, 3: down -> next QKV, 4: QKV -> o), at most l2pf_cap
+    // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
+    unsigned l2pf_mask = 0;
+    // decode: combine the attention chunks in the o-projection's B setup (1) instead of inside the
+    // attention kernel's cluster (0, default)
+    bool attn_fuse = false;
+    TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
+    int64_t l2pf_cap = 64ll << 20;
 
     template <class T>
     cudaError_t alloc(T** p, size_t count) {
@@ -110,6 +120,7 @@ struct Engine {
         for (auto& g : graphs) cudaGraphExecDestroy(g.second);
         for (void* p : allocs) cudaFree(p);
         if (trace) cudaFree(trace);
+        if (trace_buf) cudaFree(trace_buf);
         if (tok_hist) cudaFree(tok_hist);
         for (float* p : pinned)
             if (p) cudaFreeHost(p);
@@ -269,6 +280,7 @@ GemmParams gemm_base(const Engine* E, int n_out, int k, int ncols) {
     p.n_out = n_out;
     p.k = k;
     p.ncols = ncols;
+    p.trace = E->trace_buf;
     return p;
 }
 
@@ -293,7 +305,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     // which build their B operand from the f32 residual stream; bits are identical.
     const bool fuse = final_all && ncols <= 8;
     // the o-projection combines the attention chunks itself when its K-segments fall on heads
-    bool fuse_attn = fuse && E->max_chunks <= 16;
+    bool fuse_attn = fuse && E->attn_fuse && E->max_chunks <= 16;
     {
         const int S = gemm_ksplit(d, qd), nkb = qd / 64;
         for (int sg = 0; sg <= S && fuse_attn; ++sg)
@@ -308,6 +320,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         const Layer& Ly = E->layers[l];
         GemmParams g = gemm_base(E, qd + 2 * kd, d, ncols);
         g.mode = kEpiQkvRope;
+        g.trace_tag = kProfQkv;
         g.q_out = E->q;
         g.hq = c.hq;
         g.hkv = c.hkv;
@@ -327,6 +340,14 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             g.norm_gamma = Ly.attn_norm;
             g.norm_d = d;
             g.norm_eps = c.eps;
+        }
+        const int64_t wb_qkv = int64_t(qd + 2 * kd) * d * 2, wb_o = int64_t(d) * qd * 2,
+                      wb_gu = int64_t(2 * c.F) * d * 2, wb_down = int64_t(d) * c.F * 2;
+        const unsigned pf = fuse ? E->l2pf_mask : 0u;
+        auto pf_bytes = [&](int64_t b) { return b < E->l2pf_cap ? b : E->l2pf_cap; };
+        if (pf & 16u) {
+            g.l2pf = Ly.wo;
+            g.l2pf_bytes = pf_bytes(wb_o);
         }
         if (!(E->skip_mask & (1u << kProfQkv)) && (e = gemm_launch(Ly.tm_qkv, tm_h, g, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfQkv);
@@ -349,10 +370,17 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
         a.partials_only = fuse_attn ? 1 : 0;   // the o-projection GEMM combines the chunks
+        a.trace = E->trace_buf;
+        a.trace_tag = kProfAttn;
+        if (pf & 1u) {
+            a.l2pf = Ly.wo;
+            a.l2pf_bytes = pf_bytes(wb_o);
+        }
         if (!(E->skip_mask & (1u << kProfAttn)) && (e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
         GemmParams go = gemm_base(E, d, qd, ncols);
         go.mode = kEpiAddF32;
+        go.trace_tag = kProfO;
         go.out = E->x;
         go.ld_out = d;
         if (fuse) {
@@ -368,6 +396,10 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             go.attn_max_chunks = E->max_chunks;
             go.attn_chunk = kAttnChunk;
         }
+        if (pf & 2u) {
+            go.l2pf = Ly.wgu;
+            go.l2pf_bytes = pf_bytes(wb_gu);
+        }
         if (!(E->skip_mask & (1u << kProfO)) && (e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);
         if (!fuse) {
@@ -379,6 +411,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         }
         GemmParams gu = gemm_base(E, 2 * c.F, d, ncols);
         gu.mode = kEpiSwiglu;
+        gu.trace_tag = kProfGateUp;
         gu.act = E->act;
         if (fuse) {
             gu.norm_x = E->x;
@@ -387,15 +420,24 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             gu.norm_d = d;
             gu.norm_eps = c.eps;
         }
+        if (pf & 4u) {
+            gu.l2pf = Ly.wdown;
+            gu.l2pf_bytes = pf_bytes(wb_down);
+        }
         if (!(E->skip_mask & (1u << kProfGateUp)) && (e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfGateUp);
         GemmParams gd = gemm_base(E, d, c.F, ncols);
         gd.mode = kEpiAddF32;
+        gd.trace_tag = kProfDown;
         gd.out = E->x;
         gd.ld_out = d;
         if (fuse) {
             gd.ss_out = E->norm_ss;
             gd.ss_tiles = d / 128;
+        }
+        if ((pf & 8u) && l + 1 < c.L) {
+            gd.l2pf = E->layers[l + 1].wqkv;
+            gd.l2pf_bytes = pf_bytes(wb_qkv);
         }
         if (!(E->skip_mask & (1u << kProfDown)) && (e = gemm_launch(Ly.tm_down, tm_act, gd, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfDown);
@@ -428,6 +470,7 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
     if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
     GemmParams g = gemm_base(E, c.V, c.d, ncols);
     g.mode = kEpiStoreF32;
+    g.trace_tag = kProfLmHead;
     if (fuse_norm) {   // final RMSNorm fused into the lm_head's B operand (decode, <= 8 columns)
         g.norm_x = E->x;
         g.norm_ss = E->norm_ss;
@@ -746,6 +789,8 @@ int detgpu_create(int device, const char* model_id, const char* arch, uint32_t m
     E->arch = arch;
     E->max_batch = std::max<uint32_t>(1, std::min<uint32_t>(max_batch, 256));
     E->max_context = std::max<uint32_t>(1, max_context);
+    if (const char* v = std::getenv("DETGPU_L2PF")) E->l2pf_mask = static_cast<unsigned>(std::strtoul(v, nullptr, 0));
+    if (const char* v = std::getenv("DETGPU_L2PF_MB")) E->l2pf_cap = std::strtoll(v, nullptr, 0) << 20;
     cudaSetDevice(device);
     Engine* Ep = E.get();
     {
@@ -930,6 +975,49 @@ extern "C" {
 // classes in skip_mask left out (bit k = class k of detgpu_profile_decode_step), replay it `reps`
 // times and return the mean ms per step. Numerically meaningless when skip_mask != 0; never used
 // by generate().
+int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
+    if (h == nullptr || name == nullptr) return fail(nullptr, DETGPU_EINVAL, "set_option: null argument");
+    Engine* E = h->e.get();
+    if (std::strcmp(name, "l2pf_mask") == 0) E->l2pf_mask = static_cast<unsigned>(value);
+    else if (std::strcmp(name, "l2pf_cap_mb") == 0) E->l2pf_cap = value << 20;
+    else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
+    else if (std::strcmp(name, "attn_fuse") == 0) E->attn_fuse = value != 0;
+    else if (std::strcmp(name, "trace") == 0) {
+        cudaSetDevice(E->device);
+        if (E->trace_buf != nullptr) cudaFree(E->trace_buf);
+        E->trace_buf = nullptr;
+        if (value > 0) {
+            const uint32_t cap = static_cast<uint32_t>(value < (1 << 24) ? value : (1 << 24));
+            ENG_CUDA(cudaMalloc(&E->trace_buf, sizeof(TraceRec) * (cap + 1)));
+            const uint32_t hdr[2] = {0u, cap};
+            ENG_CUDA(cudaMemcpy(E->trace_buf, hdr, sizeof(hdr), cudaMemcpyHostToDevice));
+        }
+    }
+    else return fail(E, DETGPU_EINVAL, std::string("set_option: unknown option '") + name + "'");
+    cudaSetDevice(E->device);
+    for (auto& kv : E->graphs) cudaGraphExecDestroy(kv.second);
+    E->graphs.clear();
+    return DETGPU_OK;
+}
+
+int detgpu_trace_read(detgpu_engine* h, void* out, uint32_t max_records, uint32_t* n_records) {
+    if (h == nullptr || n_records == nullptr) return fail(nullptr, DETGPU_EINVAL, "trace_read: null argument");
+    Engine* E = h->e.get();
+    *n_records = 0;
+    if (E->trace_buf == nullptr) return fail(E, DETGPU_EINVAL, "trace_read: tracing is off");
+    cudaSetDevice(E->device);
+    ENG_CUDA(cudaStreamSynchronize(E->stream));
+    uint32_t hdr[2];
+    ENG_CUDA(cudaMemcpy(hdr, E->trace_buf, sizeof(hdr), cudaMemcpyDeviceToHost));
+    const uint32_t n = std::min(std::min(hdr[0], hdr[1]), max_records);
+    if (out != nullptr && n > 0)
+        ENG_CUDA(cudaMemcpy(out, E->trace_buf + 1, sizeof(TraceRec) * n, cudaMemcpyDeviceToHost));
+    *n_records = n;
+    hdr[0] = 0;
+    ENG_CUDA(cudaMemcpy(E->trace_buf, hdr, sizeof(uint32_t), cudaMemcpyHostToDevice));
+    return DETGPU_OK;
+}
+
 int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t skip_mask, uint32_t reps,
                          float* ms_per_step) {
     if (h == nullptr || h->e->toy) return fail(nullptr, DETGPU_EINVAL, "profile: transformer engine required");

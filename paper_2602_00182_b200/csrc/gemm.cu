@@ -24,6 +24,7 @@ constexpr int SUB_N = 64;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int B_BYTES = SUB_N * BK * 2;     // 8 KB
 constexpr int kMaxBc = 35;                  // k-blocks of a fused B buffer
+constexpr int kRecvBytes = 4096;            // push combine: (S-1) peers x owned columns x 128 rows x f32
 
 template <int NSUB>
 struct Cfg {
@@ -33,8 +34,10 @@ struct Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + NSUB * B_BYTES;
     static constexpr int BUDGET = NSUB <= 2 ? 96 * 1024 : 192 * 1024;
     static constexpr int STAGES = BUDGET / STAGE_BYTES;
-    // one-column-group decode: 10 KB more so the fused B buffer (the B ring + this) holds 35 k-blocks
+    // one-column-group decode: 10 KB more: 6 KB so the fused B buffer (the B ring + this) holds 35
+    // k-blocks, then the 4 KB receive buffer of the pushed K-segment partials (kRecvBytes)
     static constexpr int BC_EXTRA = NSUB == 1 ? 10 * 1024 : 0;
+    static constexpr int RECV_OFF = STAGES * NSUB * B_BYTES + 6 * 1024;   // from sB
     static constexpr int SMEM = STAGES * STAGE_BYTES + BC_EXTRA + 1024 /*align*/ + 640 /*barriers*/;
     static constexpr int MIN_CTAS = NSUB <= 2 ? 2 : 1;
     static constexpr uint32_t TMEM = NSUB * SUB_N;   // f32 accumulator columns (power of two)
@@ -46,7 +49,7 @@ __device__ __forceinline__ float epilogue_store(const GemmParams& p, int row, in
             int64_t off;
             if (p.col_step != nullptr) {
                 const int st = p.col_step[col];
-                if (st < 0) return;
+                if (st < 0) return v;
                 off = static_cast<int64_t>(p.col_slot[col]) * p.slot_stride + static_cast<int64_t>(st) * p.n_out;
             } else {
                 off = static_cast<int64_t>(col) * p.ld_out;
@@ -108,6 +111,27 @@ __device__ __forceinline__ float epilogue_any(const GemmParams& p, int row, int 
         return v;
     }
     return epilogue_store(p, row, col, v);
+}
+
+// Decode: while the accumulator builds, touch what the epilogue of (row, col) will read so those
+// loads hit L1 afterwards (the residual for AddF32; RoPE tables and the page table for QKV).
+__device__ __forceinline__ void epilogue_prefetch(const GemmParams& p, int row, int col) {
+    if (p.mode == kEpiAddF32) {
+        prefetch_l1(p.out + static_cast<int64_t>(col) * p.ld_out + row);
+    } else if (p.mode == kEpiQkvRope) {
+        const int pos = p.col_pos[col];
+        if (pos < 0) return;
+        const int qrows = p.hq * p.hd, krows = p.hkv * p.hd;
+        if (row < qrows + krows) {
+            const int64_t i = static_cast<int64_t>(pos) * (p.hd / 2) + (row % p.hd) / 2;
+            prefetch_l1(p.rope_cos + i);
+            prefetch_l1(p.rope_sin + i);
+        }
+        if (row >= qrows) prefetch_l1(p.block_table + static_cast<int64_t>(p.col_req[col]) * p.max_pages + pos / p.page);
+    } else if (p.mode == kEpiStoreF32 && p.col_step != nullptr) {
+        prefetch_l1(p.col_step + col);
+        prefetch_l1(p.col_slot + col);
+    }
 }
 
 __device__ __forceinline__ void epi_bar();
@@ -184,96 +208,186 @@ __device__ __forceinline__ void release_b(uint64_t* bready, int i) {
     mbar_arrive(&bready[i]);
 }
 
+// Arrive on k-blocks [released, done) of the fused B buffer (every producer thread, same sequence).
+__device__ __forceinline__ void release_b_range(uint64_t* bready, int& released, int done) {
+    if (done <= released) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int i = released; i < done; ++i) mbar_arrive(&bready[i]);
+    released = done;
+}
+
+// Items are (k-block, column, 4 consecutive k) in k-block-major order, 128 per round, so k-blocks
+// are released to the MMA as soon as their last item is stored. x and gamma of the next round are
+// in flight while the current one is converted; the sums of squares load with the first round.
 __device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready, int kb0, int nkb, int col0,
                              int ncols, int ew, int lane) {
     __shared__ float s_rstd[8];
+    constexpr int R = 4;   // items per thread per round
     const int d = p.norm_d, ntiles = d / 128;
-    for (int cc = ew; cc < ncols; cc += 4) {
-        // the producer of x left one partial per 128-row tile; their tree is the tree over d
-        const float part = lane < ntiles ? p.norm_ss[static_cast<int64_t>(col0 + cc) * ntiles + lane] : kNegZero;
-        const float ss = warp_tree_sum(part);
-        if (lane == 0) {
+    const int t = ew * 32 + lane;
+    const int per_kb = ncols * 16, total = nkb * per_kb;
+    float part[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {   // the producer of x left one partial per 128-row tile
+        const int cc = ew + 4 * j;
+        part[j] = cc < ncols && lane < ntiles ? __ldcg(p.norm_ss + static_cast<int64_t>(col0 + cc) * ntiles + lane)
+                                              : kNegZero;
+    }
+    float4 xn[R];
+    uint2 gn[R];
+    auto load = [&](int q0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int q = q0 + r * 128 + t;
+            if (q < total) {
+                const int i = q / per_kb, rem = q % per_kb, c = rem >> 4, kq = (rem & 15) * 4;
+                const int k = (kb0 + i) * BK + kq;
+                xn[r] = __ldcg(reinterpret_cast<const float4*>(p.norm_x + static_cast<int64_t>(col0 + c) * d + k));
+                gn[r] = __ldg(reinterpret_cast<const uint2*>(p.norm_gamma + k));
+            }
+        }
+    };
+    load(0);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int cc = ew + 4 * j;
+        const float ss = warp_tree_sum(part[j]);   // == the tree over d
+        if (cc < ncols && lane == 0) {
             const float ms = __fdiv_rn(ss, static_cast<float>(d));
             s_rstd[cc] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, p.norm_eps)));
         }
     }
     epi_bar();
-    // quad q = (column, k-block, 4 consecutive k): all of the segment's loads are issued at once
-    const int t = ew * 32 + lane;
-    const int per_col = nkb * 16, total = ncols * per_col;
-#pragma unroll 4
-    for (int q = t; q < total; q += 128) {
-        const int c = q / per_col, rem = q % per_col, i = rem >> 4, kq = (rem & 15) * 4;
-        const float rstd = s_rstd[c];
-        const int k = (kb0 + i) * BK + kq;
-        const float4 xv = *reinterpret_cast<const float4*>(p.norm_x + static_cast<int64_t>(col0 + c) * d + k);
-        const uint2 gv = *reinterpret_cast<const uint2*>(p.norm_gamma + k);
-        put_b(bc, i, c, kq, __fmul_rn(__fmul_rn(xv.x, rstd), __uint_as_float(gv.x << 16)),
-              __fmul_rn(__fmul_rn(xv.y, rstd), __uint_as_float(gv.x & 0xffff0000u)),
-              __fmul_rn(__fmul_rn(xv.z, rstd), __uint_as_float(gv.y << 16)),
-              __fmul_rn(__fmul_rn(xv.w, rstd), __uint_as_float(gv.y & 0xffff0000u)));
+    int released = 0;
+    for (int q0 = 0; q0 < total; q0 += R * 128) {
+        float4 xc[R];
+        uint2 gc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            xc[r] = xn[r];
+            gc[r] = gn[r];
+        }
+        if (q0 + R * 128 < total) load(q0 + R * 128);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int q = q0 + r * 128 + t;
+            if (q < total) {
+                const int i = q / per_kb, rem = q % per_kb, c = rem >> 4, kq = (rem & 15) * 4;
+                const float rstd = s_rstd[c];
+                put_b(bc, i, c, kq, __fmul_rn(__fmul_rn(xc[r].x, rstd), __uint_as_float(gc[r].x << 16)),
+                      __fmul_rn(__fmul_rn(xc[r].y, rstd), __uint_as_float(gc[r].x & 0xffff0000u)),
+                      __fmul_rn(__fmul_rn(xc[r].z, rstd), __uint_as_float(gc[r].y << 16)),
+                      __fmul_rn(__fmul_rn(xc[r].w, rstd), __uint_as_float(gc[r].y & 0xffff0000u)));
+            }
+        }
+        release_b_range(bready, released, q0 + R * 128 >= total ? nkb : (q0 + R * 128) / per_kb);
     }
-    for (int i = 0; i < nkb; ++i) release_b(bready, i);
 }
 
 // O-projection input from attention chunk partials ws[col][kvh][chunk][g][4 + hd] = (m, l, -, -, o[hd]).
+// Phase 1 (per column and head): M = max_c m_c, a_c = exp(m_c - M), L = fma chain of l_c a_c in
+// chunk order; all (m, l) loads and the positions in one round trip, the chains interleaved.
+// Phase 2: O_d = fma chain of o_cd a_c in chunk order, B = bf16(O_d / L), k-block-major with
+// progressive release as in norm_b_setup.
 __device__ void attn_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready, int kb0, int nkb, int col0,
-                             int ncols, int ew, int lane, ExpTab tab) {
-    constexpr int kMaxH = 8, kMaxC = 16;
+                             int ncols, int ew, int lane, ExpTab tab, uint64_t* tm) {
+    auto mark = [&](int i) {
+        if (tm != nullptr && ew == 0 && lane == 0) tm[i] = globaltimer_ns();
+    };
+    constexpr int kMaxH = 8, kMaxC = 16, PB = 16;   // PB: (column, head) pairs per warp
     __shared__ float s_al[8][kMaxH][kMaxC];   // combine weights a_c per (column, head)
     __shared__ float s_L[8][kMaxH];
+    __shared__ int s_nch[8];
     const int hd = p.attn_hd, G = p.attn_G, hkv = p.attn_hkv, mc = p.attn_max_chunks;
     const int h0 = kb0 * BK / hd;                            // first head of this K-segment
     const int nh = (nkb * BK + hd - 1) / hd;
+    const int npairs = ncols * nh;
     auto wsp = [&](int col, int h, int ch) {
         return p.attn_ws + ((static_cast<int64_t>(col0 + col) * hkv + h / G) * mc + ch) * G * (hd + 4) +
                (h % G) * (hd + 4);
     };
-    // per (column, head): M = max_c m_c, a_c = exp(m_c - M), L = fma chain of l_c a_c (chunk order)
-    for (int q = ew; q < ncols * nh; q += 4) {
-        const int cc = q / nh, hl = q % nh, h = h0 + hl;
-        const int pos = p.attn_pos[col0 + cc];
-        const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
-        // lane ch holds chunk ch's (m, l); the chain runs on shuffled registers, in chunk order
-        const float m = lane < nch ? __ldcg(wsp(cc, h, lane)) : -FLT_MAX;
-        const float l = lane < nch ? __ldcg(wsp(cc, h, lane) + 1) : 0.0f;
-        const float M = warp_max(m);
-        const float al = det_expf_shfl(lane < nch ? __fsub_rn(m, M) : 0.0f, tab);   // all lanes
-        if (lane < nch) s_al[cc][hl][lane] = al;
-        float L = 0.0f;
-        for (int ch = 0; ch < nch; ++ch)
-            L = __fmaf_rn(__shfl_sync(0xffffffffu, l, ch), __shfl_sync(0xffffffffu, al, ch), L);
-        if (lane == 0) s_L[cc][hl] = L;
-    }
-    epi_bar();
-    const int t = ew * 32 + lane;
-    const int per_col = nkb * 16, total = ncols * per_col;
-#pragma unroll 2
-    for (int q = t; q < total; q += 128) {
-        const int c = q / per_col, rem = q % per_col, i = rem >> 4, kq = (rem & 15) * 4;
-        const int pos = p.attn_pos[col0 + c];
-        const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
-        const int k = (kb0 + i) * BK + kq;   // input feature = head * hd + d
-        const int h = k / hd, hl = h - h0, dd = k % hd;
-        float4 ov[kMaxC];
+    const int posl = lane < ncols ? p.attn_pos[col0 + lane] : -1;
+    float m[PB], l[PB], al[PB], L[PB];
+    int nchj[PB];
 #pragma unroll
-        for (int ch = 0; ch < kMaxC; ++ch)   // all loads in flight before the chain
-            if (ch < nch) ov[ch] = __ldcg(reinterpret_cast<const float4*>(wsp(c, h, ch) + 4 + dd));
-        float O0 = 0.0f, O1 = 0.0f, O2 = 0.0f, O3 = 0.0f;
-#pragma unroll
-        for (int ch = 0; ch < kMaxC; ++ch) {
-            if (ch < nch) {
-                const float a = s_al[c][hl][ch];
-                O0 = __fmaf_rn(ov[ch].x, a, O0);
-                O1 = __fmaf_rn(ov[ch].y, a, O1);
-                O2 = __fmaf_rn(ov[ch].z, a, O2);
-                O3 = __fmaf_rn(ov[ch].w, a, O3);
-            }
+    for (int j = 0; j < PB; ++j) {   // chunk slots beyond a column's count are masked below
+        const int q = ew + 4 * j;
+        m[j] = -FLT_MAX;
+        l[j] = 0.0f;
+        if (q < npairs && lane < mc) {
+            const float* w = wsp(q / nh, h0 + q % nh, lane);
+            m[j] = __ldcg(w);
+            l[j] = __ldcg(w + 1);
         }
-        const float L = s_L[c][hl];
-        put_b(bc, i, c, kq, __fdiv_rn(O0, L), __fdiv_rn(O1, L), __fdiv_rn(O2, L), __fdiv_rn(O3, L));
     }
-    for (int i = 0; i < nkb; ++i) release_b(bready, i);
+    int maxnch = 0;
+    mark(9);
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+        const int q = ew + 4 * j;
+        nchj[j] = 0;
+        al[j] = 0.0f;
+        L[j] = 0.0f;
+        if (q < npairs) {   // warp-uniform
+            const int cc = q / nh, hl = q % nh;
+            const int pos = __shfl_sync(0xffffffffu, posl, cc);
+            const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
+            nchj[j] = nch;
+            maxnch = max(maxnch, nch);
+            const float mj = lane < nch ? m[j] : -FLT_MAX;
+            const float M = warp_max(mj);
+            al[j] = det_expf_shfl(lane < nch ? __fsub_rn(mj, M) : 0.0f, tab);   // all lanes
+            if (lane < nch) s_al[cc][hl][lane] = al[j];
+        }
+    }
+    mark(10);
+    for (int ch = 0; ch < maxnch; ++ch) {
+#pragma unroll
+        for (int j = 0; j < PB; ++j) {
+            const float lc = __shfl_sync(0xffffffffu, l[j], ch), ac = __shfl_sync(0xffffffffu, al[j], ch);
+            if (ch < nchj[j]) L[j] = __fmaf_rn(lc, ac, L[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+        const int q = ew + 4 * j;
+        if (q < npairs && lane == 0) s_L[q / nh][q % nh] = L[j];
+    }
+    if (ew == 0 && lane < ncols) s_nch[lane] = posl < 0 ? 0 : (posl + p.attn_chunk) / p.attn_chunk;
+    mark(11);
+    epi_bar();
+    mark(12);
+    const int t = ew * 32 + lane;
+    const int per_kb = ncols * 16, total = nkb * per_kb;
+    int released = 0;
+    for (int q0 = 0; q0 < total; q0 += 128) {
+        const int q = q0 + t;
+        if (q < total) {
+            const int i = q / per_kb, rem = q % per_kb, c = rem >> 4, kq = (rem & 15) * 4;
+            const int nch = s_nch[c];
+            const int k = (kb0 + i) * BK + kq;   // input feature = head * hd + d
+            const int h = k / hd, hl = h - h0, dd = k % hd;
+            float4 ov[kMaxC];
+#pragma unroll
+            for (int ch = 0; ch < kMaxC; ++ch)   // all loads in flight before the chain
+                if (ch < nch) ov[ch] = __ldcg(reinterpret_cast<const float4*>(wsp(c, h, ch) + 4 + dd));
+            float O0 = 0.0f, O1 = 0.0f, O2 = 0.0f, O3 = 0.0f;
+#pragma unroll
+            for (int ch = 0; ch < kMaxC; ++ch) {
+                if (ch < nch) {
+                    const float a = s_al[c][hl][ch];
+                    O0 = __fmaf_rn(ov[ch].x, a, O0);
+                    O1 = __fmaf_rn(ov[ch].y, a, O1);
+                    O2 = __fmaf_rn(ov[ch].z, a, O2);
+                    O3 = __fmaf_rn(ov[ch].w, a, O3);
+                }
+            }
+            const float Lc = s_L[c][hl];
+            put_b(bc, i, c, kq, __fdiv_rn(O0, Lc), __fdiv_rn(O1, Lc), __fdiv_rn(O2, Lc), __fdiv_rn(O3, Lc));
+        }
+        if (q0 == 0) mark(13);
+        release_b_range(bready, released, q0 + 128 >= total ? nkb : (q0 + 128) / per_kb);
+    }
 }
 
 // Grid (S, n_out/128, column groups), cluster (S,1,1): the S CTAs of a cluster own the same 128
@@ -295,9 +409,13 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* bready = tfull + 1;        // [kMaxBc] fused B: k-block i ready (128 producer arrivals)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bready + kMaxBc);
+    uint64_t* recv_bar = bready + kMaxBc;   // push combine: peers' partials landed
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(recv_bar + 1);
 
     __shared__ float s_red[4];
+    __shared__ uint64_t s_tm[kTraceMarks];   // timeline marks (p.trace only)
+    const bool tracing = p.trace != nullptr;
+    if (tracing && threadIdx.x < kTraceMarks) s_tm[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.ksplit;
     const int seg = blockIdx.x;                 // == %cluster_ctarank
@@ -314,6 +432,13 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     const int bmode = p.norm_x != nullptr ? 1 : (p.attn_ws != nullptr ? 2 : 0);
     const bool fused = bmode != 0;
     uint8_t* bc = sB;   // fused B buffer: 1 KB per k-block (see norm_b_setup)
+    // Decode (<= 8 columns): column cl is finalised by CTA cl % S; every other segment pushes its
+    // partial of that column straight into the owner's receive buffer (st.async + mbarrier), so the
+    // owner never waits on a remote read and nobody waits for the owner.
+    const int recv_cols = (ncols + S - 1) / S;   // owned columns per CTA, at most
+    const bool push = NSUB == 1 && S > 1 && ncols <= 8 && (S - 1) * recv_cols * BM * 4 <= kRecvBytes;
+    float* recv = reinterpret_cast<float*>(sB + C::RECV_OFF);   // [peer slot][owned column][row]
+    const int owned = seg < ncols ? (ncols - 1 - seg) / S + 1 : 0;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -324,12 +449,15 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         }
         mbar_init(tfull, 1);
         for (int i = 0; i < kMaxBc; ++i) mbar_init(&bready[i], 128);
+        mbar_init(recv_bar, 1);
+        if (push && owned > 0) mbar_arrive_expect_tx(recv_bar, static_cast<uint32_t>((S - 1) * owned * BM * 4));
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tslot, C::TMEM);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (push) cluster_arrive();   // receive barriers initialised (waited on before the first push)
     const uint32_t tbase = *tslot;
 
     // Weight tile (128 rows x 64 k) through a 3D tensor map: pre-tiled weights are one contiguous
@@ -348,10 +476,16 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             load_w(sA + i * A_BYTES, &tmW, &full[i], kb0 + i);
         }
     }
+    if (warp == 3 && lane == 0)
+        l2_prefetch_slice(p.l2pf, p.l2pf_bytes, blockIdx.x + S * (blockIdx.y + gridDim.y * blockIdx.z),
+                          S * gridDim.y * gridDim.z);
+    if (bmode == 1 && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
+        for (int i = threadIdx.x - 128; i < nkb; i += 128) prefetch_l2(p.norm_gamma + (kb0 + i) * BK);
     // Every kernel waits for its predecessor before triggering its dependents, so when a kernel
     // starts, all kernels before its predecessor have completed (attention relies on this).
     pdl_wait();
     pdl_trigger();
+    if (tracing && threadIdx.x == 0) s_tm[1] = globaltimer_ns();
     if (warp == 0) {
         if (lane == 0) {
             if (!fused)
@@ -408,12 +542,56 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         const ExpTab tab = exp_tab_lane();
         if (fused) {
             if (bmode == 1) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
-            else attn_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane, tab);
+            else attn_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane, tab, tracing ? s_tm : nullptr);
+        }
+        if (tracing && threadIdx.x == 128) s_tm[2] = globaltimer_ns();   // B operand built (fused)
+        if (push) {
+#pragma unroll
+            for (int cl = 0; cl < 8; ++cl)
+                if (cl < ncols && cl % S == seg) epilogue_prefetch(p, m0 + rl, col0 + cl);
         }
         mbar_wait(tfull, 0);
         tc_fence_after();
+        if (tracing && threadIdx.x == 128) s_tm[3] = globaltimer_ns();   // accumulator complete
         float* P = reinterpret_cast<float*>(smem);   // partial tile [col][128] (stages are idle now)
-        for (int j = 0; j < nb; ++j) {
+        if (push) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + (static_cast<uint32_t>(ew * 32) << 16), r);
+            tc_wait_ld();
+            cluster_wait();
+            const uint32_t rbase = smem_u32(recv);
+#pragma unroll
+            for (int cl = 0; cl < 8; ++cl) {
+                const int o = cl % S;
+                if (cl < ncols && o != seg) {
+                    const int slot = seg < o ? seg : seg - 1;
+                    const uint32_t off = 4u * static_cast<uint32_t>((slot * recv_cols + cl / S) * BM + rl);
+                    st_async_f32(mapa_shared(rbase + off, o), __uint_as_float(r[cl]), mapa_shared(smem_u32(recv_bar), o));
+                }
+            }
+            if (tracing && threadIdx.x == 128) s_tm[4] = globaltimer_ns();   // partials pushed
+            if (owned > 0) {
+                mbar_wait(recv_bar, 0);
+                if (tracing && threadIdx.x == 128) s_tm[5] = globaltimer_ns();   // peers' partials landed
+#pragma unroll
+                for (int cl = 0; cl < 8; ++cl) {
+                    if (cl < ncols && cl % S == seg) {
+                        float v[8];
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2) {
+                            const int slot = s2 < seg ? s2 : s2 - 1;
+                            v[s2] = s2 >= S ? kNegZero
+                                  : s2 == seg ? __uint_as_float(r[cl])
+                                              : recv[(slot * recv_cols + cl / S) * BM + rl];
+                        }
+                        const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v), tab);
+                        if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, ew, lane, s_red);
+                    }
+                }
+                if (tracing && threadIdx.x == 128) s_tm[7] = globaltimer_ns();   // epilogue done
+            }
+        }
+        for (int j = 0; j < nb && !push; ++j) {
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 uint32_t r[32];
@@ -428,30 +606,72 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                             if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl0 + c, xn, ew, lane, s_red);
                         }
                 } else {
+                    float4* P4 = reinterpret_cast<float4*>(P);   // [column quad][row] x 4 columns
 #pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (cl0 + c < ncols) P[(cl0 + c) * BM + rl] = __uint_as_float(r[c]);
+                    for (int c = 0; c < 32; c += 4)
+                        P4[((cl0 + c) >> 2) * BM + rl] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                                                     __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
                 }
             }
         }
     }
-    if (S > 1) {
+    if (tracing && threadIdx.x == 128 && !push) s_tm[4] = globaltimer_ns();   // partial tile / epilogue written
+    if (push && warp < 4) cluster_wait();   // pairs the arrive above (long complete by now)
+    if (S > 1 && !push) {
         cluster_sync_all();   // partial tiles of all segments visible cluster-wide
+        if (tracing && threadIdx.x == 128) s_tm[5] = globaltimer_ns();   // cluster exchange ready
         if (warp >= 4) {
             const int rl = (warp - 4) * 32 + lane;
             const ExpTab tab = exp_tab_lane();
             const uint32_t pbase = smem_u32(smem);
-            for (int cl = seg; cl < ncols; cl += S) {
+            // CTA `seg` finalises column quads seg, seg+S, ...; QB quads per round trip so that all
+            // their DSMEM loads are in flight together.
+            constexpr int QB = NSUB <= 2 ? 1 : 2;
+            const int nq = ncols <= 8 ? 0 : (ncols + 3) >> 2;
+            for (int cl = seg; ncols <= 8 && cl < ncols; cl += S) {   // decode: one column per CTA
                 float v[8];
 #pragma unroll
                 for (int s = 0; s < 8; ++s)
-                    v[s] = s < S ? ld_dsmem_f32(mapa_shared(pbase + 4u * static_cast<uint32_t>(cl * BM + rl), s))
+                    v[s] = s < S ? ld_dsmem_f32(mapa_shared(
+                                       pbase + 16u * static_cast<uint32_t>((cl >> 2) * BM + rl) + 4u * (cl & 3), s))
                                  : kNegZero;
-                const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v), tab);
+                const float sum = local_tree_sum<8>(v);
+                if (tracing && threadIdx.x == 128 && s_tm[6] == 0) s_tm[6] = globaltimer_ns();   // DSMEM loads
+                const float xn = epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
                 if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, warp - 4, lane, s_red);
             }
+            for (int q0 = seg; q0 < nq; q0 += QB * S) {
+                float4 v[QB][8];
+#pragma unroll
+                for (int u = 0; u < QB; ++u) {
+                    const int q = q0 + u * S;
+#pragma unroll
+                    for (int s = 0; s < 8; ++s)
+                        v[u][s] = (s < S && q < nq)
+                                      ? ld_dsmem_f32x4(mapa_shared(pbase + 16u * static_cast<uint32_t>(q * BM + rl), s))
+                                      : make_float4(kNegZero, kNegZero, kNegZero, kNegZero);
+                }
+#pragma unroll
+                for (int u = 0; u < QB; ++u) {
+                    const int q = q0 + u * S;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int cl = q * 4 + e;
+                        if (q < nq && cl < ncols) {
+                            float t[8];
+#pragma unroll
+                            for (int s = 0; s < 8; ++s)
+                                t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
+                            const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(t), tab);
+                            if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, warp - 4, lane, s_red);
+                        }
+                    }
+                }
+            }
         }
+        if (tracing && threadIdx.x == 128) s_tm[7] = globaltimer_ns();   // combine + epilogue done
         cluster_sync_all();   // peers keep their shared memory until every reader is done
+        if (tracing && threadIdx.x == 128) s_tm[8] = globaltimer_ns();
     }
     tc_fence_before();
     __syncthreads();
@@ -459,6 +679,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         tc_fence_after();
         tmem_dealloc(tbase, C::TMEM);
     }
+    if (tracing && threadIdx.x == 0)
+        trace_record(p.trace, (p.trace_tag << 24) | (blockIdx.x + S * (blockIdx.y + gridDim.y * blockIdx.z)), s_tm);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -8,6 +8,7 @@
 // are the same for every batch size: a column's bits depend only on its own activations and the
 // weights (tested by tests/test_gpu_gemm.py::test_batch_invariance).
 #pragma once
+#include "trace.h"
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -64,6 +65,10 @@ struct GemmParams {
     // kEpiAddF32 in fused decode: emit the next RMSNorm's per-tile sums of squares of the result
     float* ss_out;             // [ncols][ss_tiles] or nullptr
     int ss_tiles;              // n_out / 128
+    const void* l2pf;          // optional: bytes warmed into L2 at kernel start (the next kernel's weights)
+    int64_t l2pf_bytes;
+    TraceRec* trace;    // optional per-CTA timeline (timing instrumentation)
+    uint32_t trace_tag;
 };
 
 // 3D tensor map of a weight matrix [n_out][k] (row-major view or pre-tiled, see gemm.cu load_w).

@@ -1,5 +1,6 @@
 // Non-GEMM kernels of the deterministic decode path (declarations).
 #pragma once
+#include "trace.h"
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -50,6 +51,10 @@ struct AttnParams {
     int ncols, hq, hkv, hd, page, max_pages, max_chunks;
     int decode;                    // 1: every column's positions < pos were written by earlier launches
     int partials_only;             // 1: write every chunk's (m, l, o) and stop; the o-GEMM combines
+    const void* l2pf;              // optional: bytes warmed into L2 at kernel start (the o weights)
+    int64_t l2pf_bytes;
+    TraceRec* trace;        // optional per-CTA timeline (timing instrumentation)
+    uint32_t trace_tag;
 };
 size_t attn_workspace_bytes(const AttnParams& a);
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);

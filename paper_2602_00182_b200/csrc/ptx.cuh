@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda.h>
 
+#include "trace.h"
+
 namespace detgpu {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -160,6 +162,30 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
 }
+__device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+// Split cluster barrier: every thread of every CTA arrives once (release) and waits (acquire).
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// Arrive (release, cluster scope) on an mbarrier in a peer CTA's shared memory (mapa_shared address).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+// 4 bytes into a peer CTA's shared memory; completes `bytes` on the peer's mbarrier (both addresses
+// from mapa_shared).
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "r"(__float_as_uint(v)), "r"(remote_bar)
+                 : "memory");
+}
 
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
@@ -171,5 +197,46 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------- programmatic dependent launch
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------- per-CTA timeline (tools/trace_step.py)
+// Buffer layout: u32 count, u32 capacity, then records from index 1. Timing instrumentation only.
+__device__ __forceinline__ uint32_t sm_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void trace_record(TraceRec* buf, uint32_t tag, const uint64_t* marks /* [kTraceMarks] */) {
+    if (buf == nullptr) return;
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(buf);
+    const uint32_t i = atomicAdd(hdr, 1u);
+    if (i >= hdr[1]) return;
+    TraceRec r;
+    r.tag = tag;
+    r.sm = sm_id();
+    for (int j = 0; j < kTraceMarks; ++j) r.t[j] = marks[j];
+    r.t[kTraceMarks] = globaltimer_ns();
+    buf[1 + i] = r;
+}
+
+// ---------------------------------------------------------------- L2 prefetch (bulk async)
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void* ptr) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr) : "memory");
+}
+__device__ __forceinline__ void l2_prefetch_bulk(const void* ptr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+// Part `part` of `parts` equal 16-byte-aligned slices of [base, base + bytes), issued in 64 KB pieces
+// (the next kernel's weights, warmed into L2 while this kernel runs; no effect on results).
+__device__ __forceinline__ void l2_prefetch_slice(const void* base, int64_t bytes, int part, int parts) {
+    if (base == nullptr || bytes <= 0) return;
+    const int64_t per = ((bytes + parts - 1) / parts + 15) & ~int64_t(15);
+    const int64_t b0 = static_cast<int64_t>(part) * per;
+    const int64_t b1 = b0 + per < bytes ? b0 + per : bytes;
+    for (int64_t o = b0; o < b1; o += 65536)
+        l2_prefetch_bulk(static_cast<const char*>(base) + o, static_cast<uint32_t>(b1 - o < 65536 ? b1 - o : 65536));
+}
 
 }  // namespace detgpu

@@ -243,6 +243,10 @@ class Engine:
 
     __del__ = close
 
+    def set_option(self, name: str, value: int) -> None:
+        """Scheduling knob that never changes a result bit (detgpu_set_option)."""
+        L.check(L.lib.detgpu_set_option(self.h, name.encode(), int(value)), self.h)
+
     def generate(self, prompts, policies, seeds, batch_size: Optional[int] = None, want_logits: bool = True,
                  want_hash: bool = True, device_only: bool = False):
         """Returns (tokens list[np.uint32], logits list[np.float32 [T,V]] or None, hashes list[bytes])."""
