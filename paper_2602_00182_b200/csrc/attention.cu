@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
             const int p = p0 + r;
             const int pid = __ldg(bt + r / a.page);
             const int64_t off = ((static_cast<int64_t>(pid) * a.hkv + kvh) * a.page + p % a.page) * HD;
-            cp_async_16(sK + r * HD + v * 8, a.kcache + off + v * 8);
+            cp_async_16(sK + r * HD + ((v ^ (r & (VPR - 1))) * 8), a.kcache + off + v * 8);   // swizzled
             cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
         }
     };
@@ -125,48 +125,33 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __syncthreads();
     tr.mark(2);   // K/V chunk and q in shared memory
 
-    // scores: each warp takes two positions per step; 2G butterflies interleaved
-    float q[G][E];
+    // scores: one thread per (position, head) evaluates the canonical tree over d sequentially:
+    // 8-product blocks (perfect trees) merged by a binary counter == the perfect tree over HD.
+    // K rows are stored with their 16-byte vectors XOR-swizzled by row, so the 32 rows a warp
+    // reads at one vector index fall in distinct banks.
+    {
+        constexpr int NV = HD / 8;                       // 16-byte vectors per row
+        constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
+        const float4* q4 = reinterpret_cast<const float4*>(sQ);
+        for (int idx = tid; idx < G * CH; idx += kNT) {
+            const int p = idx % CH, g = idx / CH;
+            if (p >= n) continue;
+            float stk[DEPTH];
 #pragma unroll
-    for (int g = 0; g < G; ++g)
+            for (int v = 0; v < NV; ++v) {
+                const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
+                const float4 qa = q4[(g * HD + v * 8) / 4], qb = q4[(g * HD + v * 8) / 4 + 1];
+                float pr[8] = {__fmul_rn(qa.x, __uint_as_float(kv.x << 16)), __fmul_rn(qa.y, __uint_as_float(kv.x & 0xffff0000u)),
+                               __fmul_rn(qa.z, __uint_as_float(kv.y << 16)), __fmul_rn(qa.w, __uint_as_float(kv.y & 0xffff0000u)),
+                               __fmul_rn(qb.x, __uint_as_float(kv.z << 16)), __fmul_rn(qb.y, __uint_as_float(kv.z & 0xffff0000u)),
+                               __fmul_rn(qb.z, __uint_as_float(kv.w << 16)), __fmul_rn(qb.w, __uint_as_float(kv.w & 0xffff0000u))};
+                float carry = local_tree_sum<8>(pr);
+                int lvl = 0;
 #pragma unroll
-        for (int j = 0; j < E; ++j) q[g][j] = sQ[g * HD + lane * E + j];
-    for (int p = warp * 2; p < n; p += 2 * kNW) {
-        const bool two = p + 1 < n;
-        float k0[E], k1[E];
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            k0[j] = bf2f(sK[p * HD + lane * E + j]);
-            k1[j] = two ? bf2f(sK[(p + 1) * HD + lane * E + j]) : 0.0f;
-        }
-        float s0[G], s1[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float a0[E], a1[E];
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                a0[j] = __fmul_rn(q[g][j], k0[j]);
-                a1[j] = __fmul_rn(q[g][j], k1[j]);
+                for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[lvl], carry);
+                stk[lvl] = carry;
             }
-            s0[g] = local_tree_sum<E>(a0);
-            s1[g] = local_tree_sum<E>(a1);
-        }
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                s0[g] = __fadd_rn(s0[g], __shfl_xor_sync(0xffffffffu, s0[g], off));
-                s1[g] = __fadd_rn(s1[g], __shfl_xor_sync(0xffffffffu, s1[g], off));
-            }
-        }
-        if (lane < G) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (g == lane) {
-                    sS[g * CH + p] = __fmul_rn(s0[g], scale);
-                    if (two) sS[g * CH + p + 1] = __fmul_rn(s1[g], scale);
-                }
-            }
+            sS[g * CH + p] = __fmul_rn(stk[DEPTH - 1], scale);
         }
     }
     __syncthreads();
@@ -207,8 +192,8 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
 #pragma unroll
     for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
     if (tid < CHAINS) {
-        const int d = tid % HD;   // every chain of this thread has the same d (kNT % HD == 0)
-#pragma unroll 4
+        const int d = tid % HD;
+#pragma unroll 8
         for (int p = 0; p < n; ++p) {
             const float v = bf2f(sV[p * HD + d]);
 #pragma unroll

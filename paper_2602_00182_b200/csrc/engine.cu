@@ -106,8 +106,9 @@ struct Engine {
     // decode: combine the attention chunks in the o-projection's B setup (1) instead of inside the
     // attention kernel's cluster (0, default)
     bool attn_fuse = false;
+    int self_pf_kb = 8;   // GemmParams::self_pf_kb
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
-    int64_t l2pf_cap = 64ll << 20;
+    int64_t l2pf_cap = 16ll << 20;
 
     template <class T>
     cudaError_t alloc(T** p, size_t count) {
@@ -272,8 +273,10 @@ void mark(Engine* E, int cls) {
     cudaEventRecord(ev, E->stream);
     E->prof->push_back({ev, cls});
 }
-GemmParams gemm_base(const Engine* E, int n_out, int k, int ncols) {
+GemmParams gemm_base(const Engine* E, const void* w, int n_out, int k, int ncols) {
     GemmParams p{};
+    p.w_raw = w;
+    p.self_pf_kb = E->self_pf_kb;
     p.w_tiled = 1;   // engine weights are stored pre-tiled
     p.mma_wide = 1;  // one N = 64*sub-tiles MMA per K step: column bits identical (tools/wide_mma_check.py)
 
@@ -318,7 +321,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     ++n;
     for (int l = 0; l < c.L; ++l) {
         const Layer& Ly = E->layers[l];
-        GemmParams g = gemm_base(E, qd + 2 * kd, d, ncols);
+        GemmParams g = gemm_base(E, Ly.wqkv, qd + 2 * kd, d, ncols);
         g.mode = kEpiQkvRope;
         g.trace_tag = kProfQkv;
         g.q_out = E->q;
@@ -378,7 +381,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         }
         if (!(E->skip_mask & (1u << kProfAttn)) && (e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
-        GemmParams go = gemm_base(E, d, qd, ncols);
+        GemmParams go = gemm_base(E, Ly.wo, d, qd, ncols);
         go.mode = kEpiAddF32;
         go.trace_tag = kProfO;
         go.out = E->x;
@@ -409,7 +412,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             mark(E, kProfNorm);
             ++n;
         }
-        GemmParams gu = gemm_base(E, 2 * c.F, d, ncols);
+        GemmParams gu = gemm_base(E, Ly.wgu, 2 * c.F, d, ncols);
         gu.mode = kEpiSwiglu;
         gu.trace_tag = kProfGateUp;
         gu.act = E->act;
@@ -426,7 +429,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         }
         if (!(E->skip_mask & (1u << kProfGateUp)) && (e = gemm_launch(Ly.tm_gu, tm_h, gu, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfGateUp);
-        GemmParams gd = gemm_base(E, d, c.F, ncols);
+        GemmParams gd = gemm_base(E, Ly.wdown, d, c.F, ncols);
         gd.mode = kEpiAddF32;
         gd.trace_tag = kProfDown;
         gd.out = E->x;
@@ -468,7 +471,7 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
     const ModelConfig& c = E->cfg;
     CUtensorMap tmX;
     if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
-    GemmParams g = gemm_base(E, c.V, c.d, ncols);
+    GemmParams g = gemm_base(E, E->lm_head, c.V, c.d, ncols);
     g.mode = kEpiStoreF32;
     g.trace_tag = kProfLmHead;
     if (fuse_norm) {   // final RMSNorm fused into the lm_head's B operand (decode, <= 8 columns)
@@ -982,6 +985,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "l2pf_cap_mb") == 0) E->l2pf_cap = value << 20;
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
     else if (std::strcmp(name, "attn_fuse") == 0) E->attn_fuse = value != 0;
+    else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);

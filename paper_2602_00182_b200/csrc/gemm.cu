@@ -113,25 +113,73 @@ __device__ __forceinline__ float epilogue_any(const GemmParams& p, int row, int 
     return epilogue_store(p, row, col, v);
 }
 
-// Decode: while the accumulator builds, touch what the epilogue of (row, col) will read so those
-// loads hit L1 afterwards (the residual for AddF32; RoPE tables and the page table for QKV).
-__device__ __forceinline__ void epilogue_prefetch(const GemmParams& p, int row, int col) {
+// Decode: while the accumulator builds, the epilogue warps load what the epilogue of (row, col)
+// will read (the residual for AddF32; RoPE factors and the destination for QKV; the trace slot for
+// the lm_head), so the epilogue after the last MMA has no dependent global round trip.
+struct EpiPre {
+    float a, b;     // AddF32: residual x; QKV: cos, sin
+    int64_t off;    // QKV / StoreF32: destination element offset (< 0: nothing to store)
+    int where;      // QKV: 0 q_out, 1 kcache, 2 vcache
+};
+
+__device__ __forceinline__ EpiPre epilogue_preload(const GemmParams& p, int row, int col) {
+    EpiPre e{0.0f, 0.0f, -1, 0};
     if (p.mode == kEpiAddF32) {
-        prefetch_l1(p.out + static_cast<int64_t>(col) * p.ld_out + row);
+        e.a = p.out[static_cast<int64_t>(col) * p.ld_out + row];
     } else if (p.mode == kEpiQkvRope) {
         const int pos = p.col_pos[col];
-        if (pos < 0) return;
+        if (pos < 0) return e;
+        const int qrows = p.hq * p.hd, krows = p.hkv * p.hd;
+        const int d = row % p.hd;
+        if (row < qrows + krows) {
+            const int64_t i = static_cast<int64_t>(pos) * (p.hd / 2) + (d >> 1);
+            e.a = p.rope_cos[i];
+            e.b = p.rope_sin[i];
+        }
+        if (row < qrows) {
+            e.off = static_cast<int64_t>(col) * qrows + row;
+        } else {
+            const bool is_k = row < qrows + krows;
+            const int kvh = (row - (is_k ? qrows : qrows + krows)) / p.hd;
+            const int page_id = p.block_table[static_cast<int64_t>(p.col_req[col]) * p.max_pages + pos / p.page];
+            e.off = ((static_cast<int64_t>(page_id) * p.hkv + kvh) * p.page + pos % p.page) * p.hd + d;
+            e.where = is_k ? 1 : 2;
+        }
+    } else if (p.mode == kEpiStoreF32) {
+        if (p.col_step != nullptr) {
+            const int st = p.col_step[col];
+            e.off = st < 0 ? -1 : static_cast<int64_t>(p.col_slot[col]) * p.slot_stride + static_cast<int64_t>(st) * p.n_out + row;
+        } else {
+            e.off = static_cast<int64_t>(col) * p.ld_out + row;
+        }
+    }
+    return e;
+}
+
+// epilogue_any with the preloaded operands (same arithmetic, bit for bit)
+__device__ __forceinline__ float epilogue_pre(const GemmParams& p, int row, int col, float v, const EpiPre& e,
+                                              ExpTab tab) {
+    if (p.mode == kEpiAddF32) {
+        const float r = __fadd_rn(e.a, v);
+        p.out[static_cast<int64_t>(col) * p.ld_out + row] = r;
+        return r;
+    }
+    if (p.mode == kEpiQkvRope) {
+        const float partner = __shfl_xor_sync(0xffffffffu, v, 1);
+        if (e.off < 0) return v;
         const int qrows = p.hq * p.hd, krows = p.hkv * p.hd;
         if (row < qrows + krows) {
-            const int64_t i = static_cast<int64_t>(pos) * (p.hd / 2) + (row % p.hd) / 2;
-            prefetch_l1(p.rope_cos + i);
-            prefetch_l1(p.rope_sin + i);
+            if ((row & 1) == 0) v = __fsub_rn(__fmul_rn(v, e.a), __fmul_rn(partner, e.b));
+            else v = __fadd_rn(__fmul_rn(partner, e.b), __fmul_rn(v, e.a));
         }
-        if (row >= qrows) prefetch_l1(p.block_table + static_cast<int64_t>(p.col_req[col]) * p.max_pages + pos / p.page);
-    } else if (p.mode == kEpiStoreF32 && p.col_step != nullptr) {
-        prefetch_l1(p.col_step + col);
-        prefetch_l1(p.col_slot + col);
+        (e.where == 0 ? p.q_out : e.where == 1 ? p.kcache : p.vcache)[e.off] = f2bf(v);
+        return v;
     }
+    if (p.mode == kEpiStoreF32) {
+        if (e.off >= 0) p.out[e.off] = v;
+        return v;
+    }
+    return epilogue_any(p, row, col, v, tab);
 }
 
 __device__ __forceinline__ void epi_bar();
@@ -476,9 +524,16 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             load_w(sA + i * A_BYTES, &tmW, &full[i], kb0 + i);
         }
     }
-    if (warp == 3 && lane == 0)
+    if (warp == 3 && lane == 0) {
         l2_prefetch_slice(p.l2pf, p.l2pf_bytes, blockIdx.x + S * (blockIdx.y + gridDim.y * blockIdx.z),
                           S * gridDim.y * gridDim.z);
+        // the segment is contiguous in the tiled layout: k-blocks [pre, pre + self_pf_kb) in one request
+        const int npf = min(nkb - pre, p.self_pf_kb);
+        if (p.w_tiled && p.w_raw != nullptr && npf > 0)
+            l2_prefetch_bulk(static_cast<const uint8_t*>(p.w_raw) +
+                                 (static_cast<int64_t>(blockIdx.y) * nkb_all + kb0 + pre) * A_BYTES,
+                             static_cast<uint32_t>(npf) * A_BYTES);
+    }
     if (bmode == 1 && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
         for (int i = threadIdx.x - 128; i < nkb; i += 128) prefetch_l2(p.norm_gamma + (kb0 + i) * BK);
     // Every kernel waits for its predecessor before triggering its dependents, so when a kernel
@@ -545,11 +600,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             else attn_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane, tab, tracing ? s_tm : nullptr);
         }
         if (tracing && threadIdx.x == 128) s_tm[2] = globaltimer_ns();   // B operand built (fused)
-        if (push) {
-#pragma unroll
-            for (int cl = 0; cl < 8; ++cl)
-                if (cl < ncols && cl % S == seg) epilogue_prefetch(p, m0 + rl, col0 + cl);
-        }
+        EpiPre pre{0.0f, 0.0f, -1, 0};   // the first owned column's epilogue operands (decode)
+        if (push && seg < ncols) pre = epilogue_preload(p, m0 + rl, col0 + seg);
         mbar_wait(tfull, 0);
         tc_fence_after();
         if (tracing && threadIdx.x == 128) s_tm[3] = globaltimer_ns();   // accumulator complete
@@ -584,7 +636,9 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                                   : s2 == seg ? __uint_as_float(r[cl])
                                               : recv[(slot * recv_cols + cl / S) * BM + rl];
                         }
-                        const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(v), tab);
+                        const float sum = local_tree_sum<8>(v);
+                        const float xn = cl == seg ? epilogue_pre(p, m0 + rl, col0 + cl, sum, pre, tab)
+                                                   : epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
                         if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, ew, lane, s_red);
                     }
                 }

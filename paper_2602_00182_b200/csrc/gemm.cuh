@@ -65,6 +65,9 @@ struct GemmParams {
     // kEpiAddF32 in fused decode: emit the next RMSNorm's per-tile sums of squares of the result
     float* ss_out;             // [ncols][ss_tiles] or nullptr
     int ss_tiles;              // n_out / 128
+    const void* w_raw;         // tiled weights (w_tiled): base pointer for the L2 self-prefetch below
+    int self_pf_kb;            // before the PDL wait, warm up to this many of the CTA's own weight
+                               // k-blocks beyond the shared-memory ring into L2 (0: off)
     const void* l2pf;          // optional: bytes warmed into L2 at kernel start (the next kernel's weights)
     int64_t l2pf_bytes;
     TraceRec* trace;    // optional per-CTA timeline (timing instrumentation)

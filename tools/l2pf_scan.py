@@ -1,7 +1,9 @@
-"""Decode-step graph time vs the L2 weight-warming schedule (detgpu_set_option l2pf_*).
+"""Decode-step graph time vs scheduling options (detgpu_set_option: l2pf_*, self_pf_kb, attn_fuse).
 
-  python tools/l2pf_scan.py [batch] [ctx]
+  python tools/l2pf_scan.py [batch] [ctx] [--cases JSON]
+Each case is a dict of options; unspecified options are reset to their defaults first.
 """
+import argparse
 import ctypes as C
 import json
 import sys
@@ -11,16 +13,21 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2602_00182_b200 import _lib as L  # noqa: E402
 from paper_2602_00182_b200.detcore import Engine  # noqa: E402
 
-batch = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 640
-eng = Engine("llama3-8b:bench", "b200", max_batch=max(batch, 1), max_context=768)
-cases = [(0, 64), (1, 64), (16, 64), (2, 16), (2, 32), (2, 64), (4, 16), (4, 32), (8, 16), (8, 64), (1 | 2, 32),
-         (1 | 2 | 4 | 8, 16), (1 | 2 | 4 | 8, 32), (1 | 2 | 8, 32), (1 | 8, 64), (0, 64)]
-out = []
-for mask, cap in cases:
-    eng.set_option("l2pf_mask", mask)
-    eng.set_option("l2pf_cap_mb", cap)
+DEFAULTS = {"l2pf_mask": 2, "l2pf_cap_mb": 16, "self_pf_kb": 8, "attn_fuse": 0}   # the engine defaults
+ap = argparse.ArgumentParser()
+ap.add_argument("batch", nargs="?", type=int, default=1)
+ap.add_argument("ctx", nargs="?", type=int, default=640)
+ap.add_argument("--cases", default=None)
+ap.add_argument("--reps", type=int, default=30)
+a = ap.parse_args()
+cases = json.loads(a.cases) if a.cases else [
+    {}, {"self_pf_kb": 0, "l2pf_mask": 0}, {"self_pf_kb": 4}, {"self_pf_kb": 16}, {"l2pf_mask": 0},
+    {"l2pf_cap_mb": 32}, {}]
+eng = Engine("llama3-8b:bench", "b200", max_batch=max(a.batch, 1), max_context=768)
+for case in cases:
+    opts = dict(DEFAULTS, **case)
+    for k, v in opts.items():
+        eng.set_option(k, v)
     ms = C.c_float()
-    L.check(L.lib.detgpu_profile_graph(eng.h, batch, ctx, 0, 30, C.byref(ms)), eng.h)
-    out.append({"mask": mask, "cap_mb": cap, "ms": round(ms.value, 4)})
-    print(json.dumps(out[-1]), flush=True)
+    L.check(L.lib.detgpu_profile_graph(eng.h, a.batch, a.ctx, 0, a.reps, C.byref(ms)), eng.h)
+    print(json.dumps({"batch": a.batch, "case": case, "ms": round(ms.value, 4)}), flush=True)
