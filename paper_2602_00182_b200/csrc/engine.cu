@@ -102,7 +102,8 @@ struct Engine {
     // Decode: which kernels warm the NEXT kernel's weights into L2 at their start (bit 0: attention ->
     // o, 1: o -> gate/up, 2: gate/up -> down, 3: down -> next QKV, 4: QKV -> o), at most l2pf_cap
     // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
-    unsigned l2pf_mask = 0;
+    // Default: the o-projection warms the first 16 MB of gate/up (tools/l2pf_scan.py).
+    unsigned l2pf_mask = 2;
     // decode: combine the attention chunks in the o-projection's B setup (1) instead of inside the
     // attention kernel's cluster (0, default)
     bool attn_fuse = false;
