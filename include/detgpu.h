@@ -133,6 +133,8 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *                 attention kernel's cluster (0, default)
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor
+ *   "succ_pf_slots" > 0: GEMM CTA i warms the weights of CTA i + value (its successor in the
+ *                 next wave) into L2 at its start
  *   "trace"       > 0: record a per-CTA timeline of the decode kernels (capacity in records), 0: off
  * Cached decode graphs are dropped. Returns DETGPU_EINVAL for an unknown name. */
 int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value);

@@ -533,6 +533,15 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             l2_prefetch_bulk(static_cast<const uint8_t*>(p.w_raw) +
                                  (static_cast<int64_t>(blockIdx.y) * nkb_all + kb0 + pre) * A_BYTES,
                              static_cast<uint32_t>(npf) * A_BYTES);
+        if (p.w_tiled && p.w_raw != nullptr && p.succ_pf_slots > 0 && blockIdx.z == 0) {
+            const int succ = blockIdx.x + S * blockIdx.y + p.succ_pf_slots;   // linear id in column group 0
+            if (succ < S * static_cast<int>(gridDim.y)) {
+                const int s2 = succ % S, t2 = succ / S;
+                const int a0 = s2 * nkb_all / S, a1 = (s2 + 1) * nkb_all / S;
+                l2_prefetch_slice(static_cast<const uint8_t*>(p.w_raw) + (static_cast<int64_t>(t2) * nkb_all + a0) * A_BYTES,
+                                  static_cast<int64_t>(a1 - a0) * A_BYTES, 0, 1);
+            }
+        }
     }
     if (bmode == 1 && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
         for (int i = threadIdx.x - 128; i < nkb; i += 128) prefetch_l2(p.norm_gamma + (kb0 + i) * BK);
