@@ -557,15 +557,19 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                     for (int j = 0; j < nb; ++j)
                         tma_load_2d(sB + (i * NSUB + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
                                     kEvictLast);
+            int s = pre % STAGES, ph = (pre / STAGES) & 1;   // ring slot and phase, advanced incrementally
             for (int i = pre; i < nkb; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                mbar_wait(&empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&full[s], stage_tx);
                 load_w(sA + s * A_BYTES, &tmW, &full[s], kb0 + i);
                 if (!fused)
                     for (int j = 0; j < nb; ++j)
                         tma_load_2d(sB + (s * NSUB + j) * B_BYTES, &tmX, &full[s], (kb0 + i) * BK,
                                     col0 + j * SUB_N, kEvictLast);
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
             }
         }
     } else if (warp == 1) {
@@ -573,10 +577,10 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             constexpr uint32_t idesc = umma_idesc_bf16(BM, SUB_N);
             const bool wide = p.mma_wide && !fused && nb > 1;
             const uint32_t idesc_wide = umma_idesc_bf16(BM, nb * SUB_N);
+            int s = 0, ph = 0;
             for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
                 if (fused) mbar_wait(&bready[i], 0);
-                mbar_wait(&full[s], (i / STAGES) & 1);
+                mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA + s * A_BYTES);
                 const uint32_t b_base = fused ? smem_u32(bc + i * 1024) : smem_u32(sB + s * NSUB * B_BYTES);
@@ -597,6 +601,10 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                     }
                 }
                 tc_commit(&empty[s]);   // frees the smem stage once these MMAs retire
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
             }
             tc_commit(tfull);           // accumulator complete
         }
