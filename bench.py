@@ -235,6 +235,18 @@ def run_ours(args, rank: int, world: int, local: int):
     e2e_max = replicas.max_over_ranks(e2e_s, local)
     e2e_value = replicas.sum_over_ranks(args.gen * args.batch * args.e2e_steps, local) / e2e_max
     replay_rate = float(np.mean([h == hashes[0] for h in hashes]))
+    # the same calls with receipt v2 (DETGPU_F_RECEIPT_V2): Merkle roots on the GPU, 32 B per step D2H
+    v2_s, v2_d2h, v2_hash_ms, v2_hashes = 0.0, 0, 0.0, []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, hs = eng.generate(prompts, pols, seeds, want_logits=False, want_hash=True, receipt_v2=True)
+        v2_s += time.perf_counter() - t0
+        v2_hashes.append(hs)
+        v2_d2h += eng.last_stats.d2h_bytes
+        v2_hash_ms += eng.last_stats.hash_ms
+    v2_max = replicas.max_over_ranks(v2_s, local)
+    e2e_v2 = replicas.sum_over_ranks(args.gen * args.batch * args.e2e_steps, local) / v2_max
     # cross-GPU receipt equality: every rank runs the same probe request (global index 0)
     _, _, probe = eng.generate([replicas.synthetic_prompt(0, args.prompt, V)], [DecodePolicy.greedy(args.gen)],
                                [replicas.request_seed(0)], want_logits=False)
@@ -284,6 +296,11 @@ def run_ours(args, rank: int, world: int, local: int):
                 "d2h_bytes_per_step": d2h // max(args.e2e_steps, 1),
                 "what": "detgpu_generate with host prompt buffers; tokens + f32 logits D2H; SHA-256 receipt",
                 "hash_ms_per_step": hash_ms / max(args.e2e_steps, 1)},
+        "e2e_receipt_v2": {"value": e2e_v2, "unit": "tok/s", "d2h_bytes_per_step": v2_d2h // max(args.e2e_steps, 1),
+                           "hash_ms_per_step": v2_hash_ms / max(args.e2e_steps, 1),
+                           "replay_match_rate": float(np.mean([h == v2_hashes[0] for h in v2_hashes])),
+                           "what": "same calls, DETGPU_F_RECEIPT_V2: per-step Merkle roots of the logits on the "
+                                   "GPU (DESIGN.md §3.9); tokens + 32 B/step D2H"},
         "roofline": {"bound": "hbm", "kernel": "gate_up_gemm (tcgen05, SwiGLU epilogue)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind, "bytes_per_launch": gu_bytes, "launch_ms": gu_launch_ms,

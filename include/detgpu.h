@@ -75,6 +75,8 @@ typedef struct detgpu_stats {
 
 /* Flags for detgpu_generate. */
 #define DETGPU_F_DEVICE_ONLY 1u /* keep tokens/logits in HBM: no D2H, no out_hash (bench `value`) */
+#define DETGPU_F_RECEIPT_V2 2u  /* out_hash = receipt v2 digest (per-step Merkle roots computed on the
+                                   GPU, see detgpu_hash_canonical_v2); logits D2H only if requested */
 
 typedef struct detgpu_engine detgpu_engine;
 
@@ -159,6 +161,14 @@ void detgpu_encode_canonical(const uint32_t* tokens, uint32_t n_tokens, const fl
 /* SHA-256 of the canonical bytes without materialising them. */
 void detgpu_hash_canonical(const uint32_t* tokens, uint32_t n_tokens, const float* logits,
                            uint32_t vocab, uint8_t out[32]);
+/* Receipt v2: root_t = Merkle root of step t's f32 logits (little-endian
+ * bytes) in 4 KiB leaves with the reference DA tree rules (da.hpp:16-20: leaf H(0x00||blob),
+ * node H(0x01||l||r), odd level pairs the last node with itself); out_hash_v2 =
+ * SHA-256("RCPTv2\0\0" || [u32 T][T tokens][u32 T][(u32 V, root_t) x T]). Host reference of what
+ * DETGPU_F_RECEIPT_V2 computes on the GPU. */
+void detgpu_step_root(const float* logits, uint32_t vocab, uint8_t out[32]);
+void detgpu_hash_canonical_v2(const uint32_t* tokens, uint32_t n_tokens, const float* logits,
+                              uint32_t vocab, uint8_t out[32]);
 /* ExecutionTuple encoding (codec.cpp:67-104, big-endian, length-prefixed); returns the size,
  * writes when out != NULL. req_hash = SHA-256 of these bytes (receipts.cpp:119). */
 size_t detgpu_encode_exec_tuple(const char* model_id, const uint8_t container_digest[32], const char* arch,
@@ -197,6 +207,7 @@ int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_polic
                     uint32_t* tokens_out, float* probs_out, int32_t* status_out, void* stream);
 /* Decode attention for `ncols` queries against a contiguous (non-paged) cache:
  *   q [ncols][hq*hd] bf16, k/v [ncols? no: per query col] -> see tests/test_gpu_kernels.py. */
+int detgpu_k_step_roots(const float* trace, int n_steps, int vocab, uint8_t* roots, void* stream);
 int detgpu_k_attention(const void* q, const void* kcache, const void* vcache, const int32_t* block_table,
                        const int32_t* col_pos, const int32_t* col_req, void* out, int ncols, int hq, int hkv,
                        int hd, int page, int max_pages, void* stream);

@@ -77,6 +77,12 @@ def ref():
                                       u32, vp]
         R.ref_bench.restype = C.c_double
         R.ref_bench.argtypes = [C.c_char_p, C.c_char_p, u32, u32, u32, i32, C.POINTER(u64)]
+        R.ref_leaf_hash.restype = None
+        R.ref_leaf_hash.argtypes = [vp, C.c_size_t, vp]
+        R.ref_node_hash.restype = None
+        R.ref_node_hash.argtypes = [vp, vp, vp]
+        R.ref_merkle_root.restype = None
+        R.ref_merkle_root.argtypes = [vp, C.c_size_t, vp]
         _ref = R
     return _ref
 
@@ -269,3 +275,50 @@ class Llama:
 
 def out_hash(tokens, logits) -> bytes:
     return hashlib.sha256(encode_canonical(tokens, logits)).digest()
+
+
+# ---- receipt v2 ----
+# Per generated step, the Merkle root of the step's f32 logits (little-endian bytes) split into
+# 4 KiB leaves, with the reference's DA tree rules (proj/include/verinf/da.hpp:16-20):
+#   leaf H(0x00 || blob) (da.cpp:27-34), node H(0x01 || l || r) (da.cpp:36-43),
+#   odd level: last hash paired with itself; empty list -> H(0x00) (da.cpp:45-61).
+# out_hash_v2 = SHA-256("RCPTv2\0\0" || [u32 T][T tokens][u32 T][(u32 V, root) x T]) (LE, like v1).
+V2_LEAF_BYTES = 4096
+V2_TAG = b"RCPTv2\x00\x00"
+
+
+def merkle_leaf(blob: bytes) -> bytes:
+    return sha256(b"\x00" + blob)
+
+
+def merkle_node(left: bytes, right: bytes) -> bytes:
+    return sha256(b"\x01" + left + right)
+
+
+def merkle_root(leaf_hashes) -> bytes:
+    level = list(leaf_hashes)
+    if not level:
+        return merkle_leaf(b"")
+    while len(level) > 1:
+        level = [merkle_node(level[i], level[i + 1] if i + 1 < len(level) else level[i])
+                 for i in range(0, len(level), 2)]
+    return level[0]
+
+
+def step_root(logits_row) -> bytes:
+    b = np.ascontiguousarray(logits_row, dtype="<f4").tobytes()
+    return merkle_root([merkle_leaf(b[i:i + V2_LEAF_BYTES]) for i in range(0, len(b), V2_LEAF_BYTES)])
+
+
+def encode_canonical_v2(tokens, logits) -> bytes:
+    t = np.ascontiguousarray(tokens, dtype="<u4")
+    T = t.size
+    lg = np.ascontiguousarray(logits, dtype="<f4").reshape(T, -1) if T else np.zeros((0, 0), "<f4")
+    out = [V2_TAG, struct.pack("<I", T), t.tobytes(), struct.pack("<I", T)]
+    for i in range(T):
+        out += [struct.pack("<I", lg.shape[1]), step_root(lg[i])]
+    return b"".join(out)
+
+
+def hash_canonical_v2(tokens, logits) -> bytes:
+    return sha256(encode_canonical_v2(tokens, logits))

@@ -12,10 +12,21 @@
 #include <vector>
 
 #include "verinf/codec.hpp"
+#include "verinf/da.hpp"
 #include "verinf/detcore.hpp"
+#include "verinf/sha256.hpp"
 
 using namespace verinf;
 using namespace verinf::detcore;
+
+// The reference's SHA-256 entry point (sha256.hpp; libsodium in the reference build), over OpenSSL.
+namespace verinf {
+Hash32 sha256(std::span<const uint8_t> data) {
+    Hash32 h;
+    SHA256(data.data(), data.size(), h.data());
+    return h;
+}
+}  // namespace verinf
 
 static DecodePolicy make_policy(int kind, int has_k, uint32_t k, int has_p, float p, uint32_t max_tokens) {
     DecodePolicy pol;
@@ -40,6 +51,25 @@ static ExecutionTuple make_exec(const char* model_id, const uint8_t* digest, con
 }
 
 extern "C" {
+
+// The reference's DA Merkle rules (da.cpp:27-61), for the receipt-v2 golden vectors.
+void ref_leaf_hash(const uint8_t* blob, size_t n, uint8_t* out) {
+    const Hash32 h = da::leaf_hash(std::span<const uint8_t>(blob, n));
+    std::memcpy(out, h.data(), 32);
+}
+void ref_node_hash(const uint8_t* l, const uint8_t* r, uint8_t* out) {
+    Hash32 a, b;
+    std::memcpy(a.data(), l, 32);
+    std::memcpy(b.data(), r, 32);
+    const Hash32 h = da::node_hash(a, b);
+    std::memcpy(out, h.data(), 32);
+}
+void ref_merkle_root(const uint8_t* leaf_hashes, size_t n, uint8_t* out) {
+    std::vector<Hash32> v(n);
+    for (size_t i = 0; i < n; ++i) std::memcpy(v[i].data(), leaf_hashes + 32 * i, 32);
+    const Hash32 h = da::merkle_root(v);
+    std::memcpy(out, h.data(), 32);
+}
 
 // Runs reference infer(); writes tokens (max_tokens), canonical bytes length, out_hash = SHA-256(
 // canonical_bytes) and req_hash = SHA-256(encode_execution_tuple). Returns 0, or 1 on

@@ -22,6 +22,7 @@ DETGPU_ENODEV = 5
 
 GREEDY, TOP_K, NUCLEUS = 0, 1, 2
 F_DEVICE_ONLY = 1
+F_RECEIPT_V2 = 2
 
 
 class Policy(C.Structure):
@@ -67,6 +68,9 @@ def _load() -> C.CDLL:
         "detgpu_canonical_size": (sz, [u32, u32]),
         "detgpu_encode_canonical": (None, [vp, u32, vp, u32, vp]),
         "detgpu_hash_canonical": (None, [vp, u32, vp, u32, vp]),
+        "detgpu_step_root": (None, [vp, u32, vp]),
+        "detgpu_hash_canonical_v2": (None, [vp, u32, vp, u32, vp]),
+        "detgpu_k_step_roots": (i32, [vp, i32, i32, vp, vp]),
         "detgpu_encode_exec_tuple": (sz, [C.c_char_p, vp, C.c_char_p, C.c_char_p, C.POINTER(Policy), u64, vp, u32, vp]),
         "detgpu_decode_exec_tuple": (i32, [vp, sz, C.c_char_p, sz, vp, C.c_char_p, sz, C.c_char_p, sz,
                                            C.POINTER(Policy), C.POINTER(u64), vp, u32, C.POINTER(u32)]),

@@ -7,6 +7,7 @@
 
 #include "common.h"
 #include "detgpu.h"
+#include "digest.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -144,6 +145,20 @@ int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_polic
     cudaFreeAsync(dpol, s);
     DETGPU_CUDA_TRY(e);
     DETGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    return DETGPU_OK;
+}
+
+// Receipt v2 kernel hook: roots[t*32..] = Merkle root of rows trace[t*V .. t*V + V) for t < n_steps.
+int detgpu_k_step_roots(const float* trace, int n_steps, int V, uint8_t* roots, void* stream) {
+    if (n_steps <= 0) return DETGPU_OK;
+    int* steps = nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&steps), sizeof(int), s));
+    DETGPU_CUDA_TRY(cudaMemcpyAsync(steps, &n_steps, sizeof(int), cudaMemcpyHostToDevice, s));
+    cudaError_t e = launch_receipt_roots(trace, int64_t(n_steps) * V, steps, 1, n_steps, V, roots, n_steps, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // n_steps lives on this stack frame
+    cudaFreeAsync(steps, s);
+    DETGPU_CUDA_TRY(e);
     return DETGPU_OK;
 }
 

@@ -18,6 +18,7 @@
 
 #include "common.h"
 #include "detgpu.h"
+#include "digest.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "model.h"
@@ -83,6 +84,9 @@ struct Engine {
     float* trace = nullptr;
     size_t trace_cap = 0;
     uint32_t* tok_hist = nullptr;
+    uint8_t* d_roots = nullptr;   // receipt v2: [slot][tcap][32] per-step Merkle roots
+    int* d_steps = nullptr;       // receipt v2: steps per slot
+    size_t roots_cap = 0;
     size_t tok_cap = 0;
     int64_t slot_stride = 0;
     int tcap = 0;
@@ -125,6 +129,8 @@ struct Engine {
         if (trace) cudaFree(trace);
         if (trace_buf) cudaFree(trace_buf);
         if (tok_hist) cudaFree(tok_hist);
+        if (d_roots) cudaFree(d_roots);
+        if (d_steps) cudaFree(d_steps);
         for (float* p : pinned)
             if (p) cudaFreeHost(p);
         for (auto e : ev)
@@ -683,7 +689,7 @@ int run_group(Engine* E, uint32_t n, const uint32_t* const* prompts, const uint3
 }
 
 int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* const* tokens_out,
-                  float* const* logits_out, uint8_t* out_hash, detgpu_stats* st) {
+                  float* const* logits_out, uint8_t* out_hash, bool v2, detgpu_stats* st) {
     const int V = E->cfg.V;
     cudaStream_t s = E->stream;
     std::vector<int> status(n);
@@ -701,12 +707,38 @@ int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* co
         if (tokens_out && tokens_out[i] && pols[i].max_tokens)
             std::memcpy(tokens_out[i], &toks[size_t(i) * E->tcap], sizeof(uint32_t) * pols[i].max_tokens);
     double copy_ms = tcopy.ms(), hash_ms = 0;
+    if (v2 && out_hash != nullptr && E->tcap > 0) {
+        // receipt v2: per-step Merkle roots of the trace on the GPU, 32 bytes per step to the host
+        Timer th;
+        const size_t need = size_t(n) * E->tcap * 32;
+        if (need > E->roots_cap) {
+            if (E->d_roots) cudaFree(E->d_roots);
+            E->d_roots = nullptr;
+            ENG_CUDA(dalloc(&E->d_roots, need));
+            E->roots_cap = need;
+        }
+        if (E->d_steps == nullptr) ENG_CUDA(dalloc(&E->d_steps, size_t(E->max_batch)));
+        std::vector<int> steps(n);
+        int tmax = 0;
+        for (uint32_t i = 0; i < n; ++i) tmax = std::max(tmax, steps[i] = static_cast<int>(pols[i].max_tokens));
+        ENG_CUDA(cudaMemcpyAsync(E->d_steps, steps.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        ENG_CUDA(launch_receipt_roots(E->trace, E->slot_stride, E->d_steps, static_cast<int>(n), tmax, V, E->d_roots,
+                                      E->tcap, s));
+        std::vector<uint8_t> roots(need);
+        ENG_CUDA(cudaMemcpyAsync(roots.data(), E->d_roots, need, cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaStreamSynchronize(s));
+        if (st) st->d2h_bytes += need;
+        for (uint32_t i = 0; i < n; ++i)
+            hash_canonical_v2_roots(&toks[size_t(i) * E->tcap], pols[i].max_tokens, &roots[size_t(i) * E->tcap * 32],
+                                    static_cast<uint32_t>(V), out_hash + 32 * size_t(i));
+        hash_ms += th.ms();
+    }
     // logits: D2H through two pinned staging buffers, hashing / copying piece k while k+1 lands
     const size_t piece = E->pinned_floats;
     for (uint32_t i = 0; i < n; ++i) {
         const uint32_t T = pols[i].max_tokens;
         const bool want_logits = logits_out && logits_out[i];
-        const bool want_hash = out_hash != nullptr;
+        const bool want_hash = out_hash != nullptr && !v2;
         if (!want_logits && !want_hash) continue;
         Sha256 sha;
         if (want_hash) {
@@ -894,7 +926,8 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
         if (!(flags & DETGPU_F_DEVICE_ONLY)) {
             uint32_t* const* to = tokens_out ? tokens_out + base : nullptr;
             float* const* lo = logits_out ? logits_out + base : nullptr;
-            if (int rc = collect_group(E, n, policies + base, to, lo, out_hash ? out_hash + 32 * size_t(base) : nullptr, stats))
+            if (int rc = collect_group(E, n, policies + base, to, lo, out_hash ? out_hash + 32 * size_t(base) : nullptr,
+                                       (flags & DETGPU_F_RECEIPT_V2) != 0, stats))
                 return rc;
         } else {
             std::vector<int> status(n);
@@ -906,7 +939,10 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
     // max_tokens == 0 requests: tokens empty, canonical bytes = [0][0]
     if (out_hash && !(flags & DETGPU_F_DEVICE_ONLY))
         for (uint32_t i = 0; i < n_req; ++i)
-            if (policies[i].max_tokens == 0) hash_canonical(nullptr, 0, nullptr, vocab, out_hash + 32 * size_t(i));
+            if (policies[i].max_tokens == 0) {
+                if (flags & DETGPU_F_RECEIPT_V2) hash_canonical_v2_roots(nullptr, 0, nullptr, vocab, out_hash + 32 * size_t(i));
+                else hash_canonical(nullptr, 0, nullptr, vocab, out_hash + 32 * size_t(i));
+            }
     (void)total;
     return DETGPU_OK;
 }

@@ -10,6 +10,10 @@
 #include "detgpu.h"
 #include "receipt.h"
 
+#include <algorithm>
+#include <array>
+#include <vector>
+
 namespace detgpu {
 
 namespace {
@@ -181,6 +185,55 @@ void hash_canonical(const uint32_t* tokens, uint32_t T, const float* logits, uin
     s.final(out);
 }
 
+// ---- receipt v2: per-step Merkle roots over 4 KiB leaves, da.cpp tree rules ----
+void merkle_leaf(const void* blob, size_t n, uint8_t out[32]) {   // H(0x00 || blob), da.cpp:27-34
+    const uint8_t tag = 0x00;
+    Sha256 s;
+    s.update(&tag, 1);
+    if (n) s.update(blob, n);
+    s.final(out);
+}
+void merkle_node(const uint8_t l[32], const uint8_t r[32], uint8_t out[32]) {   // H(0x01 || l || r)
+    const uint8_t tag = 0x01;
+    Sha256 s;
+    s.update(&tag, 1);
+    s.update(l, 32);
+    s.update(r, 32);
+    s.final(out);
+}
+void step_root(const float* logits, uint32_t V, uint8_t out[32]) {
+    const size_t bytes = 4 * size_t(V);
+    std::vector<std::array<uint8_t, 32>> level((bytes + kV2LeafBytes - 1) / kV2LeafBytes);
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(logits);
+    for (size_t j = 0; j < level.size(); ++j)
+        merkle_leaf(b + j * kV2LeafBytes, std::min<size_t>(kV2LeafBytes, bytes - j * kV2LeafBytes), level[j].data());
+    if (level.empty()) {   // da.cpp:45-46 sentinel (V = 0 never occurs)
+        merkle_leaf(nullptr, 0, out);
+        return;
+    }
+    while (level.size() > 1) {   // odd level: last node paired with itself (da.cpp:48-61)
+        std::vector<std::array<uint8_t, 32>> next((level.size() + 1) / 2);
+        for (size_t i = 0; i < next.size(); ++i)
+            merkle_node(level[2 * i].data(), level[2 * i + 1 < level.size() ? 2 * i + 1 : 2 * i].data(), next[i].data());
+        level.swap(next);
+    }
+    std::memcpy(out, level[0].data(), 32);
+}
+// SHA-256 of "RCPTv2\0\0" || [T][tokens][T][(V, root) x T], little-endian like the v1 layout.
+void hash_canonical_v2_roots(const uint32_t* tokens, uint32_t T, const uint8_t* roots, uint32_t V, uint8_t out[32]) {
+    static const char tag[8] = {'R', 'C', 'P', 'T', 'v', '2', 0, 0};
+    Sha256 s;
+    s.update(tag, 8);
+    s.update(&T, 4);
+    if (T > 0) s.update(tokens, 4 * size_t(T));
+    s.update(&T, 4);
+    for (uint32_t t = 0; t < T; ++t) {
+        s.update(&V, 4);
+        s.update(roots + 32 * size_t(t), 32);
+    }
+    s.final(out);
+}
+
 }  // namespace detgpu
 
 using namespace detgpu;
@@ -225,6 +278,14 @@ void detgpu_encode_canonical(const uint32_t* tokens, uint32_t T, const float* lo
 
 void detgpu_hash_canonical(const uint32_t* tokens, uint32_t T, const float* logits, uint32_t V, uint8_t out[32]) {
     hash_canonical(tokens, T, logits, V, out);
+}
+
+void detgpu_step_root(const float* logits, uint32_t V, uint8_t out[32]) { step_root(logits, V, out); }
+
+void detgpu_hash_canonical_v2(const uint32_t* tokens, uint32_t T, const float* logits, uint32_t V, uint8_t out[32]) {
+    std::vector<uint8_t> roots(32 * size_t(T));
+    for (uint32_t t = 0; t < T; ++t) step_root(logits + size_t(t) * V, V, roots.data() + 32 * size_t(t));
+    hash_canonical_v2_roots(tokens, T, roots.data(), V, out);
 }
 
 // codec.cpp:93-104 and encode_policy codec.cpp:67-74

@@ -21,5 +21,11 @@ private:
 
 bool sha_ni_available();
 void hash_canonical(const uint32_t* tokens, uint32_t T, const float* logits, uint32_t V, uint8_t out[32]);
+// receipt v2
+constexpr size_t kV2LeafBytes = 4096;
+void merkle_leaf(const void* blob, size_t n, uint8_t out[32]);
+void merkle_node(const uint8_t l[32], const uint8_t r[32], uint8_t out[32]);
+void step_root(const float* logits, uint32_t V, uint8_t out[32]);
+void hash_canonical_v2_roots(const uint32_t* tokens, uint32_t T, const uint8_t* roots, uint32_t V, uint8_t out[32]);
 
 }  // namespace detgpu

@@ -305,7 +305,14 @@ int toy_generate(ToyWeights& tw, uint32_t n, const uint32_t* const* prompts, con
             if (tokens_out && tokens_out[i] && T) std::memcpy(tokens_out[i], &toks[size_t(i) * tcap], 4 * size_t(T));
             if (logits_out && logits_out[i] && T)
                 std::memcpy(logits_out[i], &lg[size_t(i) * tcap * 32], 4 * size_t(T) * 32);
-            if (out_hash) hash_canonical(&toks[size_t(i) * tcap], T, &lg[size_t(i) * tcap * 32], 32, out_hash + 32 * size_t(i));
+            if (out_hash && (flags & DETGPU_F_RECEIPT_V2)) {   // v2 on the host: 32 logits = one leaf per step
+                std::vector<uint8_t> roots(32 * size_t(T));
+                for (uint32_t t = 0; t < T; ++t)
+                    step_root(&lg[(size_t(i) * tcap + t) * 32], 32, roots.data() + 32 * size_t(t));
+                hash_canonical_v2_roots(&toks[size_t(i) * tcap], T, roots.data(), 32, out_hash + 32 * size_t(i));
+            } else if (out_hash) {
+                hash_canonical(&toks[size_t(i) * tcap], T, &lg[size_t(i) * tcap * 32], 32, out_hash + 32 * size_t(i));
+            }
         }
     }
     cleanup();

@@ -215,6 +215,17 @@ def decode_execution_tuple(data: bytes) -> Optional[ExecutionTuple]:
                           prompt[:plen.value].tolist())
 
 
+def hash_canonical_v2(tokens, logits) -> bytes:
+    """Receipt v2 digest on the host (detgpu_hash_canonical_v2): what DETGPU_F_RECEIPT_V2 computes."""
+    t = np.ascontiguousarray(tokens, dtype=np.uint32)
+    T = t.size
+    lg = np.ascontiguousarray(logits, dtype=np.float32).reshape(T, -1) if T else np.zeros((0, 1), np.float32)
+    out = np.zeros(32, np.uint8)
+    L.lib.detgpu_hash_canonical_v2(t.ctypes.data if T else None, T, lg.ctypes.data if T else None, lg.shape[1],
+                                   out.ctypes.data)
+    return out.tobytes()
+
+
 def req_hash(e: ExecutionTuple) -> bytes:
     return sha256(encode_execution_tuple(e))
 
@@ -248,8 +259,9 @@ class Engine:
         L.check(L.lib.detgpu_set_option(self.h, name.encode(), int(value)), self.h)
 
     def generate(self, prompts, policies, seeds, batch_size: Optional[int] = None, want_logits: bool = True,
-                 want_hash: bool = True, device_only: bool = False):
-        """Returns (tokens list[np.uint32], logits list[np.float32 [T,V]] or None, hashes list[bytes])."""
+                 want_hash: bool = True, device_only: bool = False, receipt_v2: bool = False):
+        """Returns (tokens list[np.uint32], logits list[np.float32 [T,V]] or None, hashes list[bytes]).
+        receipt_v2: hashes are the v2 digest (per-step Merkle roots on the GPU)."""
         n = len(prompts)
         pr = [np.ascontiguousarray(p, dtype=np.uint32) for p in prompts]
         pr_ptrs = (C.POINTER(C.c_uint32) * n)(*[p.ctypes.data_as(C.POINTER(C.c_uint32)) for p in pr])
@@ -268,7 +280,8 @@ class Engine:
         stats = L.Stats()
         rc = L.lib.detgpu_generate(self.h, n, pr_ptrs, lens, pols, sd, batch_size or self.max_batch, tok_ptrs, lg_ptrs,
                                    hashes.ctypes.data_as(C.POINTER(C.c_uint8)) if hashes is not None else None,
-                                   L.F_DEVICE_ONLY if device_only else 0, C.byref(stats))
+                                   (L.F_DEVICE_ONLY if device_only else 0) | (L.F_RECEIPT_V2 if receipt_v2 else 0),
+                                   C.byref(stats))
         L.check(rc, self.h)
         self.last_stats = stats
         toks = [t[:p.max_tokens] for t, p in zip(toks, policies)]
