@@ -84,6 +84,10 @@ def build_oracle(force: bool = False) -> None:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("oracle/_ref build failed")
+        # receipts/sign/sha256 over PyNaCl's libsodium: golden-vector generation only, optional
+        r = subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref-receipts"], capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write("note: oracle/_ref/libref_receipts.so not built (golden receipts stay as committed)\n")
 
 
 if __name__ == "__main__":
