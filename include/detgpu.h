@@ -133,10 +133,9 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *   "pdl"         programmatic dependent launch on (1) / off (0)
  *   "attn_fuse"   decode: combine attention chunks in the o-projection GEMM (1) or in the
  *                 attention kernel's cluster (0, default)
+ *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor
- *   "succ_pf_slots" > 0: GEMM CTA i warms the weights of CTA i + value (its successor in the
- *                 next wave) into L2 at its start
  *   "trace"       > 0: record a per-CTA timeline of the decode kernels (capacity in records), 0: off
  * Cached decode graphs are dropped. Returns DETGPU_EINVAL for an unknown name. */
 int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value);

@@ -112,7 +112,7 @@ struct Engine {
     // attention kernel's cluster (0, default)
     bool attn_fuse = false;
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
-    int succ_pf_slots = 0;   // GemmParams::succ_pf_slots
+    int max_nsub = 0;     // GemmParams::max_nsub
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
     int64_t l2pf_cap = 16ll << 20;
 
@@ -285,7 +285,7 @@ GemmParams gemm_base(const Engine* E, const void* w, int n_out, int k, int ncols
     GemmParams p{};
     p.w_raw = w;
     p.self_pf_kb = E->self_pf_kb;
-    p.succ_pf_slots = E->succ_pf_slots;
+    p.max_nsub = E->max_nsub;
     p.w_tiled = 1;   // engine weights are stored pre-tiled
     p.mma_wide = 1;  // one N = 64*sub-tiles MMA per K step: column bits identical (tools/wide_mma_check.py)
 
@@ -1025,7 +1025,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
     else if (std::strcmp(name, "attn_fuse") == 0) E->attn_fuse = value != 0;
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
-    else if (std::strcmp(name, "succ_pf_slots") == 0) E->succ_pf_slots = static_cast<int>(value);
+    else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);

@@ -467,8 +467,11 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.ksplit;
     const int seg = blockIdx.x;                 // == %cluster_ctarank
-    const int m0 = blockIdx.y * BM;
-    const int col0 = blockIdx.z * (NSUB * SUB_N);
+    // grid (S, column groups, tiles): the column groups of one weight tile run back to back, so
+    // the tile's weights are read from HBM once and from L2 by the other groups
+    const int tile = blockIdx.z, cgrp = blockIdx.y, ntiles = gridDim.z;
+    const int m0 = tile * BM;
+    const int col0 = cgrp * (NSUB * SUB_N);
     const int ncols = min(NSUB * SUB_N, p.ncols - col0);
     const int nb = (ncols + SUB_N - 1) / SUB_N;
     const int nkb_all = p.k / BK;
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     // 16 KB block per (tile, k-block) -> coordinate (0, 0, tile*nkb + kb); a plain row-major matrix
     // is viewed as [rows][K/64][64] -> coordinate (0, kb, m0). Same smem image either way.
     auto load_w = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int kb) {
-        if (p.w_tiled) tma_load_3d(dst, m, bar, 0, 0, blockIdx.y * nkb_all + kb, kEvictFirst);
+        if (p.w_tiled) tma_load_3d(dst, m, bar, 0, 0, tile * nkb_all + kb, kEvictFirst);
         else tma_load_3d(dst, m, bar, 0, kb, m0, kEvictFirst);
     };
     const uint32_t stage_tx = fused ? A_BYTES : A_BYTES + nb * B_BYTES;
@@ -525,23 +528,13 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         }
     }
     if (warp == 3 && lane == 0) {
-        l2_prefetch_slice(p.l2pf, p.l2pf_bytes, blockIdx.x + S * (blockIdx.y + gridDim.y * blockIdx.z),
-                          S * gridDim.y * gridDim.z);
+        l2_prefetch_slice(p.l2pf, p.l2pf_bytes, blockIdx.x + S * (tile + ntiles * cgrp), S * gridDim.y * gridDim.z);
         // the segment is contiguous in the tiled layout: k-blocks [pre, pre + self_pf_kb) in one request
         const int npf = min(nkb - pre, p.self_pf_kb);
         if (p.w_tiled && p.w_raw != nullptr && npf > 0)
             l2_prefetch_bulk(static_cast<const uint8_t*>(p.w_raw) +
-                                 (static_cast<int64_t>(blockIdx.y) * nkb_all + kb0 + pre) * A_BYTES,
+                                 (static_cast<int64_t>(tile) * nkb_all + kb0 + pre) * A_BYTES,
                              static_cast<uint32_t>(npf) * A_BYTES);
-        if (p.w_tiled && p.w_raw != nullptr && p.succ_pf_slots > 0 && blockIdx.z == 0) {
-            const int succ = blockIdx.x + S * blockIdx.y + p.succ_pf_slots;   // linear id in column group 0
-            if (succ < S * static_cast<int>(gridDim.y)) {
-                const int s2 = succ % S, t2 = succ / S;
-                const int a0 = s2 * nkb_all / S, a1 = (s2 + 1) * nkb_all / S;
-                l2_prefetch_slice(static_cast<const uint8_t*>(p.w_raw) + (static_cast<int64_t>(t2) * nkb_all + a0) * A_BYTES,
-                                  static_cast<int64_t>(a1 - a0) * A_BYTES, 0, 1);
-            }
-        }
     }
     if (bmode == 1 && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
         for (int i = threadIdx.x - 128; i < nkb; i += 128) prefetch_l2(p.norm_gamma + (kb0 + i) * BK);
@@ -656,7 +649,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                         const float sum = local_tree_sum<8>(v);
                         const float xn = cl == seg ? epilogue_pre(p, m0 + rl, col0 + cl, sum, pre, tab)
                                                    : epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
-                        if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, ew, lane, s_red);
+                        if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, ew, lane, s_red);
                     }
                 }
                 if (tracing && threadIdx.x == 128) s_tm[7] = globaltimer_ns();   // epilogue done
@@ -674,7 +667,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                     for (int c = 0; c < 32; ++c)
                         if (cl0 + c < ncols) {
                             const float xn = epilogue_any(p, m0 + rl, col0 + cl0 + c, __uint_as_float(r[c]), tab);
-                            if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl0 + c, xn, ew, lane, s_red);
+                            if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl0 + c, xn, ew, lane, s_red);
                         }
                 } else {
                     float4* P4 = reinterpret_cast<float4*>(P);   // [column quad][row] x 4 columns
@@ -709,7 +702,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 const float sum = local_tree_sum<8>(v);
                 if (tracing && threadIdx.x == 128 && s_tm[6] == 0) s_tm[6] = globaltimer_ns();   // DSMEM loads
                 const float xn = epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
-                if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, warp - 4, lane, s_red);
+                if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, warp - 4, lane, s_red);
             }
             for (int q0 = seg; q0 < nq; q0 += QB * S) {
                 float4 v[QB][8];
@@ -734,7 +727,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                             for (int s = 0; s < 8; ++s)
                                 t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
                             const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(t), tab);
-                            if (p.ss_out != nullptr) tile_sumsq(p, blockIdx.y, col0 + cl, xn, warp - 4, lane, s_red);
+                            if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, warp - 4, lane, s_red);
                         }
                     }
                 }
@@ -751,7 +744,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         tmem_dealloc(tbase, C::TMEM);
     }
     if (tracing && threadIdx.x == 0)
-        trace_record(p.trace, (p.trace_tag << 24) | (blockIdx.x + S * (blockIdx.y + gridDim.y * blockIdx.z)), s_tm);
+        trace_record(p.trace, (p.trace_tag << 24) | (blockIdx.x + S * (tile + ntiles * cgrp)), s_tm);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -781,7 +774,7 @@ cudaError_t launch_nsub(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.ksplit, p.n_out / BM, (p.ncols + NSUB * SUB_N - 1) / (NSUB * SUB_N));
+    cfg.gridDim = dim3(p.ksplit, (p.ncols + NSUB * SUB_N - 1) / (NSUB * SUB_N), p.n_out / BM);
     cfg.blockDim = dim3(256, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = stream;
@@ -864,7 +857,9 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     if (p.ss_out != nullptr && (p.mode != kEpiAddF32 || p.n_out != p.ss_tiles * BM || p.ncols > 8))
         return cudaErrorInvalidValue;
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
-    if (p.ncols <= 128) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
+    // > 128 columns: 128-column tiles at two CTAs per SM (one CTA's epilogue overlaps the other's
+    // main loop) beat 256-column tiles at one CTA per SM by 25 % on the 512-token prefill
+    if (p.max_nsub != 4) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
     return launch_nsub<4>(tmW, tmX, p, stream, pdl);
 }
 

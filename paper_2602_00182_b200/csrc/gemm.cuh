@@ -66,10 +66,9 @@ struct GemmParams {
     float* ss_out;             // [ncols][ss_tiles] or nullptr
     int ss_tiles;              // n_out / 128
     const void* w_raw;         // tiled weights (w_tiled): base pointer for the L2 self-prefetch below
+    int max_nsub;              // > 128 columns: widest tile in 64-column sub-tiles (4, or 0: 2)
     int self_pf_kb;            // before the PDL wait, warm up to this many of the CTA's own weight
                                // k-blocks beyond the shared-memory ring into L2 (0: off)
-    int succ_pf_slots;         // > 0: CTA i warms the weight segment of CTA i + succ_pf_slots (the CTA
-                               // that will take its slot in the next wave) into L2 at its start
     const void* l2pf;          // optional: bytes warmed into L2 at kernel start (the next kernel's weights)
     int64_t l2pf_bytes;
     TraceRec* trace;    // optional per-CTA timeline (timing instrumentation)

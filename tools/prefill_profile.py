@@ -12,8 +12,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--prompt", type=int, default=512)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--opt", action="append", default=[], help="engine option name=value (detgpu_set_option)")
 a = ap.parse_args()
 eng = Engine("llama3-8b:bench", "b200", max_batch=max(a.batch, 1), max_context=a.prompt + 2)
+for o in a.opt:
+    k, v = o.split("=")
+    eng.set_option(k, int(v))
 prompts = [replicas.synthetic_prompt(i, a.prompt, eng.vocab) for i in range(a.batch)]
 res = []
 for r in range(a.reps + 1):
@@ -21,5 +25,5 @@ for r in range(a.reps + 1):
     if r:
         res.append(eng.last_stats.prefill_ms)
 toks = a.prompt * a.batch
-print(json.dumps({"prompt": a.prompt, "batch": a.batch, "prefill_ms": res,
+print(json.dumps({"opts": a.opt, "prompt": a.prompt, "batch": a.batch, "prefill_ms": res,
                   "prefill_tok_s": toks / (min(res) / 1000), "tflops": 2 * 8.03e9 * toks / (min(res) / 1000) / 1e12}))
