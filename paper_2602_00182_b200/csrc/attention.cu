@@ -23,6 +23,138 @@ constexpr int kNT = 256;           // threads per CTA
 constexpr int kMaxClusterChunks = 16;   // cluster mode: chunks of one (column, kv head) per cluster
 constexpr int kNW = kNT / 32;
 
+// ---- the per-chunk arithmetic, shared by the chunk-parallel and the
+// chunk-sequential kernels so that both produce the same bits ----
+
+// K/V rows [r_begin, r_end) of the chunk starting at position p0 (kv head kvh) into shared memory
+// with 16-byte cp.async; K vectors XOR-swizzled by row (chunk_scores). When the page size is a
+// multiple of the chunk (the engine's 64) the chunk is one contiguous [CH][HD] block per head:
+// one page-table read per chunk instead of one per vector.
+template <int HD>
+__device__ __forceinline__ void load_chunk_rows(const AttnParams& a, const int* bt_slot, int kvh, int p0, int r_begin,
+                                                int r_end, __nv_bfloat16* sK, __nv_bfloat16* sV, bool k, bool v,
+                                                int tid) {
+    constexpr int VPR = HD * 2 / 16;
+    if (a.page % kAttnChunk == 0) {
+        const int pid = __ldg(bt_slot + p0 / a.page);
+        const int64_t base = ((static_cast<int64_t>(pid) * a.hkv + kvh) * a.page + p0 % a.page) * HD;
+        for (int i = r_begin * VPR + tid; i < r_end * VPR; i += kNT) {
+            const int r = i / VPR, vv = i % VPR;
+            const int64_t off = base + r * HD + vv * 8;
+            if (k) cp_async_16(sK + r * HD + ((vv ^ (r & (VPR - 1))) * 8), a.kcache + off);
+            if (v) cp_async_16(sV + r * HD + vv * 8, a.vcache + off);
+        }
+        return;
+    }
+    for (int i = r_begin * VPR + tid; i < r_end * VPR; i += kNT) {
+        const int r = i / VPR, vv = i % VPR;
+        const int p = p0 + r;
+        const int pid = __ldg(bt_slot + p / a.page);
+        const int64_t off = ((static_cast<int64_t>(pid) * a.hkv + kvh) * a.page + p % a.page) * HD + vv * 8;
+        if (k) cp_async_16(sK + r * HD + ((vv ^ (r & (VPR - 1))) * 8), a.kcache + off);
+        if (v) cp_async_16(sV + r * HD + vv * 8, a.vcache + off);
+    }
+}
+
+// scores: one thread per (position, head) evaluates the canonical tree over d sequentially:
+// 8-product blocks (perfect trees) merged by a binary counter == the perfect tree over HD.
+// K rows are stored with their 16-byte vectors XOR-swizzled by row, so the 32 rows a warp
+// reads at one vector index fall in distinct banks.
+template <int HD, int G>
+__device__ __forceinline__ void chunk_scores(const __nv_bfloat16* sK, const float* sQ, float* sS, int n, int tid,
+                                             float scale) {
+    constexpr int CH = kAttnChunk;
+    constexpr int NV = HD / 8;                       // 16-byte vectors per row
+    constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
+    const float4* q4 = reinterpret_cast<const float4*>(sQ);
+    for (int idx = tid; idx < G * CH; idx += kNT) {
+        const int p = idx % CH, g = idx / CH;
+        if (p >= n) continue;
+        float stk[DEPTH];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
+            const float4 qa = q4[(g * HD + v * 8) / 4], qb = q4[(g * HD + v * 8) / 4 + 1];
+            float pr[8] = {__fmul_rn(qa.x, __uint_as_float(kv.x << 16)), __fmul_rn(qa.y, __uint_as_float(kv.x & 0xffff0000u)),
+                           __fmul_rn(qa.z, __uint_as_float(kv.y << 16)), __fmul_rn(qa.w, __uint_as_float(kv.y & 0xffff0000u)),
+                           __fmul_rn(qb.x, __uint_as_float(kv.z << 16)), __fmul_rn(qb.y, __uint_as_float(kv.z & 0xffff0000u)),
+                           __fmul_rn(qb.z, __uint_as_float(kv.w << 16)), __fmul_rn(qb.w, __uint_as_float(kv.w & 0xffff0000u))};
+            float carry = local_tree_sum<8>(pr);
+            int lvl = 0;
+#pragma unroll
+            for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[lvl], carry);
+            stk[lvl] = carry;
+        }
+        sS[g * CH + p] = __fmul_rn(stk[DEPTH - 1], scale);
+    }
+}
+
+// chunk softmax pieces: warp g owns head g (CH/32 positions per lane): m, e = exp(s - m), l = tree(e)
+template <int G>
+__device__ __forceinline__ void chunk_softmax(float* sS, float* sM, float* sL, int n, int warp, int lane, ExpTab tab) {
+    constexpr int CH = kAttnChunk;
+    for (int g = warp; g < G; g += kNW) {
+        constexpr int PPL = CH / 32;   // positions per lane
+        float sv[PPL], e[PPL];
+        float m = -FLT_MAX;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int p = lane * PPL + j;
+            sv[j] = p < n ? sS[g * CH + p] : 0.0f;
+            if (p < n) m = fmaxf(m, sv[j]);
+        }
+        m = warp_max(m);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int p = lane * PPL + j;
+            const float ev = det_expf_shfl(p < n ? __fsub_rn(sv[j], m) : 0.0f, tab);
+            e[j] = p < n ? ev : kNegZero;
+            sS[g * CH + p] = e[j];
+        }
+        float l = local_tree_sum<PPL>(e);
+        l = warp_tree_sum(l);
+        if (lane == 0) {
+            sM[g] = m;
+            sL[g] = l;
+        }
+    }
+}
+
+// PV chains per thread: chain j of thread tid is chain_of(tid, j) = tid + j * kNT, i.e. head
+// ch / HD, dimension ch % HD (G * HD or more: none).
+template <int HD, int G>
+__host__ __device__ constexpr int pv_cpt() {
+    return (G * HD + kNT - 1) / kNT;
+}
+template <int HD, int G>
+__device__ __forceinline__ int chain_of(int tid, int j) {
+    return tid + j * kNT;
+}
+
+// o: chain (g, d) = fma over positions in order
+template <int HD, int G>
+__device__ __forceinline__ void chunk_pv(const __nv_bfloat16* sV, const float* sS, int n, int tid,
+                                         float (&acc)[pv_cpt<HD, G>()]) {
+    constexpr int CH = kAttnChunk;
+    constexpr int CHAINS = G * HD;
+    constexpr int CPT = pv_cpt<HD, G>();
+    const uint16_t* v16 = reinterpret_cast<const uint16_t*>(sV);
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
+    if (tid < CHAINS) {
+        const int d = tid % HD;   // every chain of this thread has the same d (kNT % HD == 0)
+#pragma unroll 8
+        for (int p = 0; p < n; ++p) {
+            const float v = __uint_as_float(static_cast<uint32_t>(v16[p * HD + d]) << 16);
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const int ch = chain_of<HD, G>(tid, j);
+                if (ch < CHAINS) acc[j] = __fmaf_rn(sS[(ch / HD) * CH + p], v, acc[j]);
+            }
+        }
+    }
+}
+
 // CL (cluster mode): the chunk CTAs of one (column, kv head) form a cluster; chunk 0 (the leader)
 // receives every other chunk's (m, l, o) by st.async into its K/V buffer once it has finished with
 // it, combines them in chunk order and writes the output: no workspace, no ticket, no grid-wide
@@ -32,7 +164,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     constexpr int CH = kAttnChunk;
     constexpr int E = HD / 32;                       // q/k elements per lane in a dot product
     constexpr int CHAINS = G * HD;                   // (head, d) accumulators of the PV product
-    constexpr int CPT = (CHAINS + kNT - 1) / kNT;    // chains per thread
+    constexpr int CPT = pv_cpt<HD, G>();            // PV chains per thread (chain_of)
     extern __shared__ __align__(16) uint8_t attn_dsm[];
     __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_dsm);
     __nv_bfloat16* sV = sK + CH * HD;
@@ -97,17 +229,9 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // K/V rows: page ids of the chunk, then every 16-byte vector with cp.async
-    constexpr int VPR = HD * 2 / 16;
-    const int* bt = a.block_table + static_cast<int64_t>(slot) * a.max_pages + p0 / a.page;
+    const int* bt = a.block_table + static_cast<int64_t>(slot) * a.max_pages;
     auto load_rows = [&](int r_begin, int r_end) {
-        for (int i = r_begin * VPR + tid; i < r_end * VPR; i += kNT) {
-            const int r = i / VPR, v = i % VPR;
-            const int p = p0 + r;
-            const int pid = __ldg(bt + r / a.page);
-            const int64_t off = ((static_cast<int64_t>(pid) * a.hkv + kvh) * a.page + p % a.page) * HD;
-            cp_async_16(sK + r * HD + ((v ^ (r & (VPR - 1))) * 8), a.kcache + off + v * 8);   // swizzled
-            cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
-        }
+        load_chunk_rows<HD>(a, bt, kvh, p0, r_begin, r_end, sK, sV, true, true, tid);
     };
     if (a.decode) {
         load_rows(0, pos - p0 < n ? pos - p0 : n);   // history rows, before the wait
@@ -125,84 +249,17 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     __syncthreads();
     tr.mark(2);   // K/V chunk and q in shared memory
 
-    // scores: one thread per (position, head) evaluates the canonical tree over d sequentially:
-    // 8-product blocks (perfect trees) merged by a binary counter == the perfect tree over HD.
-    // K rows are stored with their 16-byte vectors XOR-swizzled by row, so the 32 rows a warp
-    // reads at one vector index fall in distinct banks.
-    {
-        constexpr int NV = HD / 8;                       // 16-byte vectors per row
-        constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
-        const float4* q4 = reinterpret_cast<const float4*>(sQ);
-        for (int idx = tid; idx < G * CH; idx += kNT) {
-            const int p = idx % CH, g = idx / CH;
-            if (p >= n) continue;
-            float stk[DEPTH];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
-                const float4 qa = q4[(g * HD + v * 8) / 4], qb = q4[(g * HD + v * 8) / 4 + 1];
-                float pr[8] = {__fmul_rn(qa.x, __uint_as_float(kv.x << 16)), __fmul_rn(qa.y, __uint_as_float(kv.x & 0xffff0000u)),
-                               __fmul_rn(qa.z, __uint_as_float(kv.y << 16)), __fmul_rn(qa.w, __uint_as_float(kv.y & 0xffff0000u)),
-                               __fmul_rn(qb.x, __uint_as_float(kv.z << 16)), __fmul_rn(qb.y, __uint_as_float(kv.z & 0xffff0000u)),
-                               __fmul_rn(qb.z, __uint_as_float(kv.w << 16)), __fmul_rn(qb.w, __uint_as_float(kv.w & 0xffff0000u))};
-                float carry = local_tree_sum<8>(pr);
-                int lvl = 0;
-#pragma unroll
-                for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[lvl], carry);
-                stk[lvl] = carry;
-            }
-            sS[g * CH + p] = __fmul_rn(stk[DEPTH - 1], scale);
-        }
-    }
+    chunk_scores<HD, G>(sK, sQ, sS, n, tid, scale);
     __syncthreads();
     tr.mark(3);   // scores
 
-    // chunk softmax pieces: warp g owns head g (4 positions per lane)
     const ExpTab tab = exp_tab_lane();
-    for (int g = warp; g < G; g += kNW) {
-        constexpr int PPL = CH / 32;   // positions per lane
-        float sv[PPL], e[PPL];
-        float m = -FLT_MAX;
-#pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-            const int p = lane * PPL + j;
-            sv[j] = p < n ? sS[g * CH + p] : 0.0f;
-            if (p < n) m = fmaxf(m, sv[j]);
-        }
-        m = warp_max(m);
-#pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-            const int p = lane * PPL + j;
-            const float ev = det_expf_shfl(p < n ? __fsub_rn(sv[j], m) : 0.0f, tab);
-            e[j] = p < n ? ev : kNegZero;
-            sS[g * CH + p] = e[j];
-        }
-        float l = local_tree_sum<PPL>(e);
-        l = warp_tree_sum(l);
-        if (lane == 0) {
-            sM[g] = m;
-            sL[g] = l;
-        }
-    }
+    chunk_softmax<G>(sS, sM, sL, n, warp, lane, tab);
     __syncthreads();
     tr.mark(4);   // softmax
 
-    // o: chain (g, d) = fma over positions in order
     float acc[CPT];
-#pragma unroll
-    for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
-    if (tid < CHAINS) {
-        const int d = tid % HD;
-#pragma unroll 8
-        for (int p = 0; p < n; ++p) {
-            const float v = bf2f(sV[p * HD + d]);
-#pragma unroll
-            for (int j = 0; j < CPT; ++j) {
-                const int ch = tid + j * kNT;
-                if (ch < CHAINS) acc[j] = __fmaf_rn(sS[(ch / HD) * CH + p], v, acc[j]);
-            }
-        }
-    }
+    chunk_pv<HD, G>(sV, sS, n, tid, acc);
     tr.mark(5);   // PV chains
     const int nch = (ctx + CH - 1) / CH;
     __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
@@ -236,7 +293,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
                 __syncthreads();
 #pragma unroll
                 for (int j = 0; j < CPT; ++j) {
-                    const int ch = tid + j * kNT;
+                    const int ch = chain_of<HD, G>(tid, j);
                     if (ch >= CHAINS) continue;
                     const int g = ch / HD, d = ch % HD;
                     float L = __fmaf_rn(sL[g], s_al[g][0], 0.0f), O = __fmaf_rn(acc[j], s_al[g][0], 0.0f);
@@ -254,7 +311,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
                 const uint32_t rbar = mapa_shared(smem_u32(&s_bar[0]), 0);
 #pragma unroll
                 for (int j = 0; j < CPT; ++j) {
-                    const int ch = tid + j * kNT;
+                    const int ch = chain_of<HD, G>(tid, j);
                     if (ch < CHAINS) st_async_f32(rb + 4u * (2 * G + ch), acc[j], rbar);
                 }
                 if (tid < G) {
@@ -270,7 +327,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         // single chunk: the combine weight is exp(0) == 1 exactly
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
-            const int ch = tid + j * kNT;
+            const int ch = chain_of<HD, G>(tid, j);
             if (ch < CHAINS)
                 outp[ch] = f2bf(__fdiv_rn(__fmaf_rn(acc[j], 1.0f, 0.0f), __fmaf_rn(sL[ch / HD], 1.0f, 0.0f)));
         }
@@ -280,7 +337,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
     float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 4);
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-        const int ch = tid + j * kNT;
+        const int ch = chain_of<HD, G>(tid, j);
         if (ch < CHAINS) ws[(ch / HD) * (HD + 4) + 4 + ch % HD] = acc[j];
     }
     if (tid < G) {
