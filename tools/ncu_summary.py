@@ -41,7 +41,7 @@ def launches(path, out):
     unit = data[0]["Metric Unit"] if data else "ns"
     scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}.get(unit, 1.0)
     for d in data:
-        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("detgpu::<unnamed>::", "").replace("unnamed>::", "")
         agg[name][0] += 1
         agg[name][1] += float(d["Metric Value"]) * scale
     tot = sum(v[1] for v in agg.values())
@@ -61,7 +61,8 @@ def full(rep, out, json_out=None):
     hdr, units = rows[0], rows[1]
     recs = []
     for r in rows[2:]:
-        rec = {"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")}
+        rec = {"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("detgpu::<unnamed>::", "")
+               .replace("unnamed>::", "")}
         for m, short in FULL_METRICS:
             if m in hdr:
                 i = hdr.index(m)
