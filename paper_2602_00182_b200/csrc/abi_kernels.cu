@@ -139,7 +139,13 @@ int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_polic
     sp.scratch = keys;
     sp.token_out = tokens_out;
     sp.status = status_out;
+    // the engine's small-batch multi-CTA path (used when rows <= kSampleMultiMaxRows)
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sp.blk_ws), sizeof(float) * 4 * kSampleMaxBlocks * rows, s));
+    DETGPU_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sp.tickets), sizeof(int) * rows, s));
+    DETGPU_CUDA_TRY(cudaMemsetAsync(sp.tickets, 0, sizeof(int) * rows, s));
     cudaError_t e = launch_sample(sp, s, false);
+    cudaFreeAsync(sp.blk_ws, s);
+    cudaFreeAsync(sp.tickets, s);
     cudaFreeAsync(keys, s);
     if (probs_out == nullptr) cudaFreeAsync(probs, s);
     cudaFreeAsync(dpol, s);

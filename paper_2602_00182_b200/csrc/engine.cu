@@ -80,6 +80,8 @@ struct Engine {
     DevPolicy* d_pol = nullptr;
     float* probs = nullptr;
     uint64_t* sort_scratch = nullptr;
+    float* sample_ws = nullptr;     // multi-CTA sampler: per-row block max / subtree sums
+    int* sample_tickets = nullptr;
     // outputs (grown on demand)
     float* trace = nullptr;
     size_t trace_cap = 0;
@@ -265,6 +267,9 @@ int init_buffers(Engine* E) {
     ENG_CUDA(E->alloc(&E->d_pol, B));
     ENG_CUDA(E->alloc(&E->probs, size_t(B) * c.V));
     ENG_CUDA(E->alloc(&E->sort_scratch, size_t(B) * c.V));
+    ENG_CUDA(E->alloc(&E->sample_ws, size_t(4) * kSampleMaxBlocks * B));
+    ENG_CUDA(E->alloc(&E->sample_tickets, size_t(B)));
+    ENG_CUDA(cudaMemset(E->sample_tickets, 0, sizeof(int) * B));
     std::vector<int> ident(B);
     for (int i = 0; i < B; ++i) ident[i] = i;
     ENG_CUDA(cudaMemcpy(E->d_req, ident.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
@@ -508,6 +513,8 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
     sp.prng = E->d_prng;
     sp.probs = E->probs;
     sp.scratch = E->sort_scratch;
+    sp.blk_ws = E->sample_ws;
+    sp.tickets = E->sample_tickets;
     sp.token_out = reinterpret_cast<uint32_t*>(E->d_tok);
     sp.status = E->d_status;
     sp.tokens_hist = E->tok_hist;
@@ -516,7 +523,7 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
     sp.col_step_mut = E->d_step;
     e = launch_sample(sp, E->stream, E->use_pdl);
     mark(E, kProfSample);
-    if (nlaunch) *nlaunch += 2;
+    if (nlaunch) *nlaunch += 2 + ((c.V + 4095) / 4096 > 1 && ncols <= kSampleMultiMaxRows ? 2 : 0);   // lm_head, sampler
     return e;
 }
 

@@ -51,6 +51,54 @@ __device__ float block_tree_sum_1024(int n, Load ld, float* s_tiles) {
     return r;
 }
 
+// The same tree when producing a leaf needs a global load followed by a store (the softmax exp
+// pass): fetch(i, ok) only loads, map(i, ok, raw) computes / stores and returns the leaf. The next
+// tile's loads are issued before this tile's stores, so loads are not serialised behind stores
+// the compiler cannot prove disjoint.
+template <class Fetch, class Map>
+__device__ float block_tree_sum_1024_fm(int n, Fetch fetch, Map map, float* s_tiles) {
+    const int P2 = max(128, next_pow2(n));
+    const int ntiles = P2 / 128;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float nxt[4];
+    if (warp < ntiles) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = warp * 128 + lane * 4 + j;
+            nxt[j] = fetch(i, i < n);
+        }
+    }
+    for (int t = warp; t < ntiles; t += 32) {
+        float raw[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) raw[j] = nxt[j];
+        if (t + 32 < ntiles) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int i = (t + 32) * 128 + lane * 4 + j;
+                nxt[j] = fetch(i, i < n);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = t * 128 + lane * 4 + j;
+            v[j] = map(i, i < n, raw[j]);   // called by every lane (warp-uniform), -0 when !valid
+        }
+        float s = local_tree_sum<4>(v);
+        s = warp_tree_sum(s);
+        if (lane == 0) s_tiles[t] = s;
+    }
+    __syncthreads();
+    for (int w = 1; w < ntiles; w <<= 1) {
+        for (int i = threadIdx.x * 2 * w; i < ntiles; i += blockDim.x * 2 * w)
+            s_tiles[i] = __fadd_rn(s_tiles[i], s_tiles[i + w]);
+        __syncthreads();
+    }
+    const float r = s_tiles[0];
+    __syncthreads();
+    return r;
+}
+
 // ------------------------------------------------------------------ RMSNorm
 // y_i = bf16((x_i * rstd) * gamma_i), rstd = 1 / sqrt(tree(x*x)/d + eps)
 template <int E>
@@ -376,98 +424,29 @@ struct SampleSmem {
     uint64_t kval;
 };
 
-__global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
-    __shared__ SampleSmem sm;
-    pdl_wait();
-    pdl_trigger();
-    const int r = blockIdx.x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    int slot = r, step = 0;
-    if (sp.col_step != nullptr) {
-        step = sp.col_step[r];
-        if (step < 0) return;
-        slot = sp.col_slot[r];
-    }
-    const DevPolicy pol = sp.policy[slot];
-    const int V = sp.vocab;
-    const float* L = sp.col_step != nullptr
-                         ? sp.logits + static_cast<int64_t>(slot) * sp.slot_stride + static_cast<int64_t>(step) * V
-                         : sp.logits + static_cast<int64_t>(r) * sp.logit_row_stride;
-    float* P = sp.probs + static_cast<int64_t>(r) * V;
-    uint64_t* sorted = sp.scratch + static_cast<int64_t>(r) * V;
-
-    // pass 1: max (left scan order is irrelevant for max) + finiteness (detcore.cpp:127-133)
-    float m = -FLT_MAX;
-    int bad = 0;
-    for (int i = tid; i < V; i += 1024) {
-        const float v = L[i];
-        if (!isfinite(v)) bad = 1;
-        m = fmaxf(m, v);
-    }
-    m = warp_max(m);
-    bad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) {
-        sm.red_f[warp] = m;
-        sm.red_i[warp] = bad;
-    }
-    if (tid == 0) sm.flag = 0;
-    __syncthreads();
-    if (warp == 0) {
-        float mm = sm.red_f[lane];
-        int bb = sm.red_i[lane];
-        mm = warp_max(mm);
-        bb = __any_sync(0xffffffffu, bb);
-        if (lane == 0) {
-            sm.fval = mm;
-            sm.flag = bb;
-        }
-    }
-    __syncthreads();
-    const float maxv = sm.fval;
-    // one generator step per token, drawn before the policy branch (detcore.cpp:256-262)
-    float rdraw = 0.0f;
-    if (tid == 0) {
-        uint64_t* st = sp.prng + static_cast<int64_t>(slot) * 4;
-        uint64_t s[4] = {st[0], st[1], st[2], st[3]};
-        const uint64_t u = xoshiro_next(s);
-        st[0] = s[0];
-        st[1] = s[1];
-        st[2] = s[2];
-        st[3] = s[3];
-        rdraw = __fmul_rn(static_cast<float>(u >> 40), 0x1.0p-24f);
-    }
-    if (sm.flag) {
-        if (tid == 0) {
-            sp.status[slot] = DETGPU_ENONFINITE;
-            sp.token_out[r] = 0;
-            if (sp.col_step_mut != nullptr) {
-                sp.col_step_mut[r] = -1;
-                sp.col_pos[r] = -1;
+// The row's tail (detcore.cpp:202-262): p_i = e_i / S, argmax, top-k / nucleus selection, one
+// token, bookkeeping. P holds e_i on entry. Called by one 1024-thread CTA per row.
+// p_i = e_i / S over [i_begin, i_end) in place, and the CTA's argmax with the smallest-index
+// tie-break (detcore.cpp:202-208); the result is valid in thread 0 (and warp 0).
+__device__ __forceinline__ void sample_divide_argmax(SampleSmem& sm, float* P, float S, int i_begin, int i_end,
+                                                     int tid, int warp, int lane, float& bp, int& bi) {
+    bp = -1.0f;
+    bi = 0x7fffffff;
+    for (int i0 = i_begin + tid; i0 < i_end; i0 += 8 * 1024) {   // 8 loads in flight before the stores
+        float e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e[u] = i0 + u * 1024 < i_end ? P[i0 + u * 1024] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * 1024;   // increasing per thread: the first maximum is kept
+            if (i < i_end) {
+                const float p = __fdiv_rn(e[u], S);
+                P[i] = p;
+                if (p > bp) {
+                    bp = p;
+                    bi = i;
+                }
             }
-        }
-        return;
-    }
-
-    // pass 2: e_i = exp(l_i - max); S = canonical tree of e
-    const ExpTab tab = exp_tab_lane();
-    const float S = block_tree_sum_1024(
-        V,
-        [&](int i, bool ok) {
-            const float e = det_expf_shfl(ok ? __fsub_rn(L[i], maxv) : 0.0f, tab);
-            if (!ok) return kNegZero;
-            P[i] = e;
-            return e;
-        },
-        sm.tiles);
-    // pass 3: p_i = e_i / S ; argmax with smallest-index tie-break (detcore.cpp:202-208)
-    float bp = -1.0f;
-    int bi = 0x7fffffff;
-    for (int i = tid; i < V; i += 1024) {
-        const float p = __fdiv_rn(P[i], S);
-        P[i] = p;
-        if (p > bp) {
-            bp = p;
-            bi = i;
         }
     }
 #pragma unroll
@@ -498,7 +477,16 @@ __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
             }
         }
     }
-    int token = bi;   // valid in thread 0
+}
+
+// The row's tail (detcore.cpp:202-262) once P holds the probabilities and thread 0 the argmax:
+// top-k / nucleus selection, one token, bookkeeping. One 1024-thread CTA per row.
+__device__ __forceinline__ void sample_tail(const SampleParams& sp, SampleSmem& sm, int r, int slot, int step,
+                                            const DevPolicy& pol, int V, float* P, uint64_t* sorted, int argmax,
+                                            float rdraw, int tid, int warp, int lane) {
+    (void)warp;
+    (void)lane;
+    int token = argmax;   // valid in thread 0
     int32_t err = DETGPU_OK;
 
     if (pol.kind != DETGPU_GREEDY) {
@@ -640,6 +628,283 @@ __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
     }
 }
 
+__device__ __forceinline__ float sample_draw(const SampleParams& sp, int slot) {   // one xoshiro step per token
+    uint64_t* st = sp.prng + static_cast<int64_t>(slot) * 4;
+    uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+    const uint64_t u = xoshiro_next(s);
+    st[0] = s[0];
+    st[1] = s[1];
+    st[2] = s[2];
+    st[3] = s[3];
+    return __fmul_rn(static_cast<float>(u >> 40), 0x1.0p-24f);
+}
+
+__device__ __forceinline__ void sample_fail_nonfinite(const SampleParams& sp, int r, int slot) {
+    sp.status[slot] = DETGPU_ENONFINITE;
+    sp.token_out[r] = 0;
+    if (sp.col_step_mut != nullptr) {
+        sp.col_step_mut[r] = -1;
+        sp.col_pos[r] = -1;
+    }
+}
+
+__global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
+    __shared__ SampleSmem sm;
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int slot = r, step = 0;
+    if (sp.col_step != nullptr) {
+        step = sp.col_step[r];
+        if (step < 0) return;
+        slot = sp.col_slot[r];
+    }
+    const DevPolicy pol = sp.policy[slot];
+    const int V = sp.vocab;
+    const float* L = sp.col_step != nullptr
+                         ? sp.logits + static_cast<int64_t>(slot) * sp.slot_stride + static_cast<int64_t>(step) * V
+                         : sp.logits + static_cast<int64_t>(r) * sp.logit_row_stride;
+    float* P = sp.probs + static_cast<int64_t>(r) * V;
+    uint64_t* sorted = sp.scratch + static_cast<int64_t>(r) * V;
+
+    // pass 1: max (left scan order is irrelevant for max) + finiteness (detcore.cpp:127-133)
+    float m = -FLT_MAX;
+    int bad = 0;
+    for (int i = tid; i < V; i += 1024) {
+        const float v = L[i];
+        if (!isfinite(v)) bad = 1;
+        m = fmaxf(m, v);
+    }
+    m = warp_max(m);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        sm.red_f[warp] = m;
+        sm.red_i[warp] = bad;
+    }
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+    if (warp == 0) {
+        float mm = sm.red_f[lane];
+        int bb = sm.red_i[lane];
+        mm = warp_max(mm);
+        bb = __any_sync(0xffffffffu, bb);
+        if (lane == 0) {
+            sm.fval = mm;
+            sm.flag = bb;
+        }
+    }
+    __syncthreads();
+    const float maxv = sm.fval;
+    // one generator step per token, drawn before the policy branch (detcore.cpp:256-262)
+    const float rdraw = tid == 0 ? sample_draw(sp, slot) : 0.0f;
+    if (sm.flag) {
+        if (tid == 0) sample_fail_nonfinite(sp, r, slot);
+        return;
+    }
+
+    // pass 2: e_i = exp(l_i - max); S = canonical tree of e
+    const ExpTab tab = exp_tab_lane();
+    const float S = block_tree_sum_1024_fm(
+        V, [&](int i, bool ok) { return ok ? L[i] : 0.0f; },
+        [&](int i, bool ok, float l) {
+            const float e = det_expf_shfl(ok ? __fsub_rn(l, maxv) : 0.0f, tab);
+            if (!ok) return kNegZero;
+            P[i] = e;
+            return e;
+        },
+        sm.tiles);
+    float bp;
+    int bi;
+    sample_divide_argmax(sm, P, S, 0, V, tid, warp, lane, bp, bi);
+    sample_tail(sp, sm, r, slot, step, pol, V, P, sorted, bi, rdraw, tid, warp, lane);
+}
+
+// Small batches: the row is split over nblk CTAs of kSampleBlock logits (aligned subtrees of the
+// canonical tree over next_pow2(V)). sample_max_kernel leaves each block's max and finiteness;
+// sample_multi_kernel computes e_i and the block's subtree sum, the last block of the row (a
+// ticket) folds the subtree sums with the same tree into S; sample_div_kernel divides and takes
+// block argmaxes, its last block reduces them and runs sample_tail. Bits equal the single-CTA
+// kernel's; the exp and divide passes run on nblk SMs instead of one.
+constexpr int kSampleBlock = 4096;
+
+__global__ void __launch_bounds__(256) sample_max_kernel(const SampleParams sp) {
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x, r = blockIdx.y;
+    int slot = r, step = 0;
+    if (sp.col_step != nullptr) {
+        step = sp.col_step[r];
+        if (step < 0) return;
+        slot = sp.col_slot[r];
+    }
+    const int V = sp.vocab;
+    const float* L = sp.col_step != nullptr
+                         ? sp.logits + static_cast<int64_t>(slot) * sp.slot_stride + static_cast<int64_t>(step) * V
+                         : sp.logits + static_cast<int64_t>(r) * sp.logit_row_stride;
+    float m = -FLT_MAX;
+    int bad = 0;
+    const int i1 = min(V, (b + 1) * kSampleBlock);
+    for (int i = b * kSampleBlock + threadIdx.x; i < i1; i += 256) {
+        const float v = L[i];
+        if (!isfinite(v)) bad = 1;
+        m = fmaxf(m, v);
+    }
+    __shared__ float rm[8];
+    __shared__ int rb[8];
+    m = warp_max(m);
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        rm[threadIdx.x >> 5] = m;
+        rb[threadIdx.x >> 5] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            m = fmaxf(m, rm[w]);
+            bad |= rb[w];
+        }
+        float* ws = sp.blk_ws + (static_cast<int64_t>(r) * kSampleMaxBlocks + b) * 4;
+        ws[0] = m;
+        ws[1] = bad ? 1.0f : 0.0f;
+    }
+}
+
+__global__ void __launch_bounds__(1024) sample_multi_kernel(const SampleParams sp) {
+    __shared__ SampleSmem sm;
+    __shared__ int s_last;
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x, r = blockIdx.y, nblk = gridDim.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int slot = r, step = 0;
+    if (sp.col_step != nullptr) {
+        step = sp.col_step[r];
+        if (step < 0) return;
+        slot = sp.col_slot[r];
+    }
+    const DevPolicy pol = sp.policy[slot];
+    const int V = sp.vocab;
+    const float* L = sp.col_step != nullptr
+                         ? sp.logits + static_cast<int64_t>(slot) * sp.slot_stride + static_cast<int64_t>(step) * V
+                         : sp.logits + static_cast<int64_t>(r) * sp.logit_row_stride;
+    float* P = sp.probs + static_cast<int64_t>(r) * V;
+    float* ws = sp.blk_ws + static_cast<int64_t>(r) * kSampleMaxBlocks * 4;
+    if (warp == 0) {   // lane j reads block j: one round trip (max is order-free)
+        float mj = lane < nblk ? __ldcg(ws + 4 * lane) : -FLT_MAX;
+        const int bj = __any_sync(0xffffffffu, lane < nblk && __ldcg(ws + 4 * lane + 1) != 0.0f);
+        mj = warp_max(mj);
+        if (lane == 0) {
+            sm.fval = mj;
+            sm.flag = bj;
+        }
+    }
+    __syncthreads();
+    const float m = sm.fval;
+    const int bad = sm.flag;
+    __syncthreads();
+    if (bad) {   // block 0 reports, with the row's one generator step
+        if (b == 0 && tid == 0) {
+            sample_draw(sp, slot);
+            sample_fail_nonfinite(sp, r, slot);
+        }
+        return;
+    }
+
+    const ExpTab tab = exp_tab_lane();
+    const int i0 = b * kSampleBlock;
+    const int nloc = max(0, min(kSampleBlock, V - i0));
+    const float part = block_tree_sum_1024_fm(
+        nloc, [&](int i, bool ok) { return ok ? L[i0 + i] : 0.0f; },
+        [&](int i, bool ok, float l) {
+            const float e = det_expf_shfl(ok ? __fsub_rn(l, m) : 0.0f, tab);
+            if (!ok) return kNegZero;
+            P[i0 + i] = e;
+            return e;
+        },
+        sm.tiles);
+    if (tid == 0) {
+        ws[4 * b + 2] = part;
+        __threadfence();
+        const int prev = atomicAdd(sp.tickets + r, 1);
+        s_last = prev == nblk - 1;
+        if (s_last) sp.tickets[r] = 0;   // re-armed for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // S: the subtree sums folded by the same perfect tree (absent subtrees are -0)
+    const int nbp = max(128, next_pow2(V)) / min(max(128, next_pow2(V)), kSampleBlock);
+    if (tid < 32) {
+        float v = tid < nblk ? __ldcg(ws + 4 * tid + 2) : kNegZero;
+        for (int off = 1; off < nbp; off <<= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, v, off);
+            v = __fadd_rn(v, o);
+        }
+        if (tid == 0) sm.fval = v;
+    }
+    if (tid == 0) ws[3] = sm.fval;   // S for sample_div_kernel
+}
+
+// p_i = e_i / S over the block, block argmax; the last block of the row reduces the block
+// candidates (smallest index on ties, as the sequential scan) and runs sample_tail.
+__global__ void __launch_bounds__(1024) sample_div_kernel(const SampleParams sp) {
+    __shared__ SampleSmem sm;
+    __shared__ int s_last;
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x, r = blockIdx.y, nblk = gridDim.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int slot = r, step = 0;
+    if (sp.col_step != nullptr) {
+        step = sp.col_step[r];
+        if (step < 0) return;
+        slot = sp.col_slot[r];
+    }
+    float* ws = sp.blk_ws + static_cast<int64_t>(r) * kSampleMaxBlocks * 4;
+    if (warp == 0) {   // non-finite row: reported by sample_multi_kernel
+        const int bj = __any_sync(0xffffffffu, lane < nblk && __ldcg(ws + 4 * lane + 1) != 0.0f);
+        if (lane == 0) sm.flag = bj;
+    }
+    __syncthreads();
+    if (sm.flag) return;
+    const DevPolicy pol = sp.policy[slot];
+    const int V = sp.vocab;
+    float* P = sp.probs + static_cast<int64_t>(r) * V;
+    const float S = __ldcg(ws + 3);
+    float bp;
+    int bi;
+    sample_divide_argmax(sm, P, S, b * kSampleBlock, min(V, (b + 1) * kSampleBlock), tid, warp, lane, bp, bi);
+    if (tid == 0) {
+        ws[4 * b + 0] = bp;   // the block max slot is free again
+        reinterpret_cast<int*>(ws)[4 * b + 2] = bi;
+        __threadfence();
+        const int prev = atomicAdd(sp.tickets + r, 1);
+        s_last = prev == nblk - 1;
+        if (s_last) sp.tickets[r] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        bp = lane < nblk ? __ldcg(ws + 4 * lane) : -1.0f;
+        bi = lane < nblk ? __ldcg(reinterpret_cast<const int*>(ws) + 4 * lane + 2) : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (op > bp || (op == bp && oi < bi)) {
+                bp = op;
+                bi = oi;
+            }
+        }
+    }
+    __syncthreads();
+    uint64_t* sorted = sp.scratch + static_cast<int64_t>(r) * V;
+    const float rdraw = tid == 0 ? sample_draw(sp, slot) : 0.0f;
+    sample_tail(sp, sm, r, slot, step, pol, V, P, sorted, bi, rdraw, tid, warp, lane);
+}
+
 cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStream_t stream, cudaLaunchAttribute* attr,
                             bool pdl) {
     cudaLaunchConfig_t cfg{};
@@ -723,6 +988,19 @@ size_t sample_scratch_bytes(int rows, int vocab) { return sizeof(uint64_t) * sta
 
 cudaError_t launch_sample(const SampleParams& sp, cudaStream_t stream, bool pdl) {
     if (sp.vocab > 131072 || sp.vocab <= 0) return cudaErrorInvalidValue;
+    const int nblk = (sp.vocab + kSampleBlock - 1) / kSampleBlock;
+    if (sp.blk_ws != nullptr && sp.tickets != nullptr && nblk > 1 && sp.rows <= kSampleMultiMaxRows) {
+        cudaLaunchAttribute a1[1], a2[1];
+        cudaLaunchConfig_t c1 = make_cfg(dim3(nblk, sp.rows), dim3(256), 0, stream, a1, pdl);
+        cudaError_t e = cudaLaunchKernelEx(&c1, sample_max_kernel, sp);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t c2 = make_cfg(dim3(nblk, sp.rows), dim3(1024), 0, stream, a2, pdl);
+        e = cudaLaunchKernelEx(&c2, sample_multi_kernel, sp);
+        if (e != cudaSuccess) return e;
+        cudaLaunchAttribute a3[1];
+        cudaLaunchConfig_t c3 = make_cfg(dim3(nblk, sp.rows), dim3(1024), 0, stream, a3, pdl);
+        return cudaLaunchKernelEx(&c3, sample_div_kernel, sp);
+    }
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = make_cfg(dim3(sp.rows), dim3(1024), 0, stream, attr, pdl);
     return cudaLaunchKernelEx(&cfg, sample_kernel, sp);

@@ -93,7 +93,12 @@ struct SampleParams {
     int tcap;
     int* col_pos;
     int* col_step_mut;
+    // small batches (rows <= kSampleMultiMaxRows, nullable): the row is split over several CTAs
+    float* blk_ws;              // [rows][kSampleMaxBlocks][4] block max / non-finite / subtree sum
+    int* tickets;               // [rows], zero-initialised; reset by the last block
 };
+constexpr int kSampleMaxBlocks = 32;   // vocab <= 32 * 4096
+constexpr int kSampleMultiMaxRows = 16;
 size_t sample_scratch_bytes(int rows, int vocab);
 cudaError_t launch_sample(const SampleParams& sp, cudaStream_t stream, bool pdl);
 

@@ -176,8 +176,9 @@ def test_softmax_decode_bit_exact(V):
     assert tok[0] == 3
 
 
-def test_sampler_nonfinite_is_reported():
-    logits = np.zeros((2, 4096), dtype=np.float32)
+@pytest.mark.parametrize("V", [4096, 128256])
+def test_sampler_nonfinite_is_reported(V):
+    logits = np.zeros((2, V), dtype=np.float32)
     logits[1, 17] = np.nan
     tok, probs, state, status = _sample(logits, [(0, None, None), (0, None, None)], [1, 2])
     assert status[0] == 0 and status[1] != 0
