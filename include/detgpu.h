@@ -77,6 +77,8 @@ typedef struct detgpu_stats {
 #define DETGPU_F_DEVICE_ONLY 1u /* keep tokens/logits in HBM: no D2H, no out_hash (bench `value`) */
 #define DETGPU_F_RECEIPT_V2 2u  /* out_hash = receipt v2 digest (per-step Merkle roots computed on the
                                    GPU, see detgpu_hash_canonical_v2); logits D2H only if requested */
+#define DETGPU_F_CONTINUOUS 4u  /* continuous batching: batch_size decode slots stay busy, each
+                                   request admitted as soon as a slot frees (same bytes per request) */
 
 typedef struct detgpu_engine detgpu_engine;
 

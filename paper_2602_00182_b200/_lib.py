@@ -23,6 +23,7 @@ DETGPU_ENODEV = 5
 GREEDY, TOP_K, NUCLEUS = 0, 1, 2
 F_DEVICE_ONLY = 1
 F_RECEIPT_V2 = 2
+F_CONTINUOUS = 4
 
 
 class Policy(C.Structure):

@@ -481,7 +481,13 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
 }
 
 // lm_head over `ncols` columns of X (tmX) into the trace at (slot, d_step[col]), then the sampler.
-cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64_t* nlaunch, bool fuse_norm = false) {
+// col_step / col_slot: the trace step and slot of each column (default: the decode state, one
+// column per slot); by_slot: the sampler updates the decode state of the column's slot (compact
+// columns of newly admitted requests in continuous batching).
+cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64_t* nlaunch, bool fuse_norm = false,
+                            const int* col_step = nullptr, const int* col_slot = nullptr, bool by_slot = false) {
+    if (col_step == nullptr) col_step = E->d_step;
+    if (col_slot == nullptr) col_slot = E->d_req;
     const ModelConfig& c = E->cfg;
     CUtensorMap tmX;
     if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
@@ -496,16 +502,17 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
         g.norm_eps = c.eps;
     }
     g.out = E->trace;
-    g.col_step = E->d_step;
-    g.col_slot = E->d_req;
+    g.col_step = col_step;
+    g.col_slot = col_slot;
     g.slot_stride = E->slot_stride;
     cudaError_t e = gemm_launch(E->tm_lm, tmX, g, E->stream, E->use_pdl);
     if (e != cudaSuccess) return e;
     mark(E, kProfLmHead);
     SampleParams sp{};
     sp.logits = E->trace;
-    sp.col_step = E->d_step;
-    sp.col_slot = E->d_req;
+    sp.col_step = col_step;
+    sp.col_slot = col_slot;
+    sp.state_by_slot = by_slot ? 1 : 0;
     sp.slot_stride = E->slot_stride;
     sp.rows = ncols;
     sp.vocab = c.V;
@@ -695,66 +702,59 @@ int run_group(Engine* E, uint32_t n, const uint32_t* const* prompts, const uint3
     return DETGPU_OK;
 }
 
-int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* const* tokens_out,
-                  float* const* logits_out, uint8_t* out_hash, bool v2, detgpu_stats* st) {
+// Outputs of one finished slot: status, tokens, logits (D2H through two pinned staging buffers,
+// hashing piece k while k+1 lands) and out_hash (v1: SHA-256 of the canonical bytes; v2: the
+// per-step Merkle roots computed on the GPU).
+int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* logits_out, uint8_t* out_hash, bool v2,
+                 detgpu_stats* st) {
     const int V = E->cfg.V;
     cudaStream_t s = E->stream;
-    std::vector<int> status(n);
-    ENG_CUDA(cudaMemcpy(status.data(), E->d_status, sizeof(int) * n, cudaMemcpyDeviceToHost));
-    for (uint32_t i = 0; i < n; ++i) {
-        if (status[i] == DETGPU_ENONFINITE) return fail(E, DETGPU_EINVAL, "det_softmax: non-finite value");
-        if (status[i] != 0) return fail(E, DETGPU_EINVAL, "decode: zero probability mass after truncation");
-    }
+    int status = 0;
+    ENG_CUDA(cudaMemcpy(&status, E->d_status + slot, sizeof(int), cudaMemcpyDeviceToHost));
+    if (status == DETGPU_ENONFINITE) return fail(E, DETGPU_EINVAL, "det_softmax: non-finite value");
+    if (status != 0) return fail(E, DETGPU_EINVAL, "decode: zero probability mass after truncation");
     Timer tcopy;
-    std::vector<uint32_t> toks(size_t(n) * std::max(E->tcap, 1));
-    if (E->tcap > 0)
-        ENG_CUDA(cudaMemcpy(toks.data(), E->tok_hist, sizeof(uint32_t) * size_t(n) * E->tcap, cudaMemcpyDeviceToHost));
-    if (st) st->d2h_bytes += sizeof(uint32_t) * size_t(n) * E->tcap;
-    for (uint32_t i = 0; i < n; ++i)
-        if (tokens_out && tokens_out[i] && pols[i].max_tokens)
-            std::memcpy(tokens_out[i], &toks[size_t(i) * E->tcap], sizeof(uint32_t) * pols[i].max_tokens);
+    std::vector<uint32_t> toks(std::max<uint32_t>(T, 1));
+    if (T > 0)
+        ENG_CUDA(cudaMemcpy(toks.data(), E->tok_hist + size_t(slot) * E->tcap, sizeof(uint32_t) * T,
+                            cudaMemcpyDeviceToHost));
+    if (st) st->d2h_bytes += sizeof(uint32_t) * size_t(T);
+    if (tokens_out && T) std::memcpy(tokens_out, toks.data(), sizeof(uint32_t) * T);
     double copy_ms = tcopy.ms(), hash_ms = 0;
-    if (v2 && out_hash != nullptr && E->tcap > 0) {
-        // receipt v2: per-step Merkle roots of the trace on the GPU, 32 bytes per step to the host
+    if (v2 && out_hash != nullptr) {
         Timer th;
-        const size_t need = size_t(n) * E->tcap * 32;
-        if (need > E->roots_cap) {
-            if (E->d_roots) cudaFree(E->d_roots);
-            E->d_roots = nullptr;
-            ENG_CUDA(dalloc(&E->d_roots, need));
-            E->roots_cap = need;
+        std::vector<uint8_t> roots(32 * size_t(std::max<uint32_t>(T, 1)));
+        if (T > 0) {
+            const size_t need = 32 * size_t(T);
+            if (need > E->roots_cap) {
+                if (E->d_roots) cudaFree(E->d_roots);
+                E->d_roots = nullptr;
+                ENG_CUDA(dalloc(&E->d_roots, std::max(need, size_t(E->max_batch) * E->tcap * 32)));
+                E->roots_cap = std::max(need, size_t(E->max_batch) * E->tcap * 32);
+            }
+            if (E->d_steps == nullptr) ENG_CUDA(dalloc(&E->d_steps, size_t(E->max_batch)));
+            const int steps = static_cast<int>(T);
+            ENG_CUDA(cudaMemcpyAsync(E->d_steps, &steps, sizeof(int), cudaMemcpyHostToDevice, s));
+            ENG_CUDA(launch_receipt_roots(E->trace + size_t(slot) * E->slot_stride, E->slot_stride, E->d_steps, 1, steps,
+                                          V, E->d_roots, E->tcap, s));
+            ENG_CUDA(cudaMemcpyAsync(roots.data(), E->d_roots, need, cudaMemcpyDeviceToHost, s));
+            ENG_CUDA(cudaStreamSynchronize(s));
+            if (st) st->d2h_bytes += need;
         }
-        if (E->d_steps == nullptr) ENG_CUDA(dalloc(&E->d_steps, size_t(E->max_batch)));
-        std::vector<int> steps(n);
-        int tmax = 0;
-        for (uint32_t i = 0; i < n; ++i) tmax = std::max(tmax, steps[i] = static_cast<int>(pols[i].max_tokens));
-        ENG_CUDA(cudaMemcpyAsync(E->d_steps, steps.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
-        ENG_CUDA(launch_receipt_roots(E->trace, E->slot_stride, E->d_steps, static_cast<int>(n), tmax, V, E->d_roots,
-                                      E->tcap, s));
-        std::vector<uint8_t> roots(need);
-        ENG_CUDA(cudaMemcpyAsync(roots.data(), E->d_roots, need, cudaMemcpyDeviceToHost, s));
-        ENG_CUDA(cudaStreamSynchronize(s));
-        if (st) st->d2h_bytes += need;
-        for (uint32_t i = 0; i < n; ++i)
-            hash_canonical_v2_roots(&toks[size_t(i) * E->tcap], pols[i].max_tokens, &roots[size_t(i) * E->tcap * 32],
-                                    static_cast<uint32_t>(V), out_hash + 32 * size_t(i));
+        hash_canonical_v2_roots(toks.data(), T, roots.data(), static_cast<uint32_t>(V), out_hash);
         hash_ms += th.ms();
     }
-    // logits: D2H through two pinned staging buffers, hashing / copying piece k while k+1 lands
-    const size_t piece = E->pinned_floats;
-    for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t T = pols[i].max_tokens;
-        const bool want_logits = logits_out && logits_out[i];
-        const bool want_hash = out_hash != nullptr && !v2;
-        if (!want_logits && !want_hash) continue;
+    const bool want_hash = out_hash != nullptr && !v2;
+    if (logits_out != nullptr || want_hash) {
+        const size_t piece = E->pinned_floats;
         Sha256 sha;
         if (want_hash) {
             sha.update(&T, 4);
-            if (T) sha.update(&toks[size_t(i) * E->tcap], 4 * size_t(T));
+            if (T) sha.update(toks.data(), 4 * size_t(T));
             sha.update(&T, 4);
         }
         const size_t total = size_t(T) * V;
-        const float* src = E->trace + size_t(i) * E->slot_stride;
+        const float* src = E->trace + size_t(slot) * E->slot_stride;
         size_t done = 0;
         int buf = 0;
         size_t inflight = std::min(piece, total);
@@ -773,7 +773,7 @@ int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* co
             }
             Timer th;
             const float* hp = E->pinned[buf];
-            if (want_logits) std::memcpy(logits_out[i] + done, hp, sizeof(float) * cur);
+            if (logits_out) std::memcpy(logits_out + done, hp, sizeof(float) * cur);
             if (want_hash) {
                 // step boundaries inside this piece: each step is prefixed by its u32 vocab size
                 size_t off = 0;
@@ -791,11 +791,174 @@ int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* co
             buf ^= 1;
         }
         if (st) st->d2h_bytes += 4 * total;
-        if (want_hash) sha.final(out_hash + 32 * size_t(i));
+        if (want_hash) sha.final(out_hash);
     }
     if (st) {
         st->d2h_ms += static_cast<float>(copy_ms);
         st->hash_ms += static_cast<float>(hash_ms);
+    }
+    return DETGPU_OK;
+}
+
+int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* const* tokens_out,
+                  float* const* logits_out, uint8_t* out_hash, bool v2, detgpu_stats* st) {
+    for (uint32_t i = 0; i < n; ++i) {
+        if (pols[i].max_tokens == 0) continue;   // handled by the caller (empty canonical output)
+        if (int rc = collect_slot(E, static_cast<int>(i), pols[i].max_tokens, tokens_out ? tokens_out[i] : nullptr,
+                                  logits_out ? logits_out[i] : nullptr, out_hash ? out_hash + 32 * size_t(i) : nullptr,
+                                  v2, st))
+            return rc;
+    }
+    return DETGPU_OK;
+}
+
+// Continuous batching: `slots` decode slots stay busy; a request is admitted into a
+// slot as soon as one frees, its prompt prefilled between decode steps and its first token sampled
+// from compact columns that update the slot's decode state. Every column is computed
+// independently of the others, so a request's bytes do not depend on what it shares
+// a step with: outputs equal the static-group path's bit for bit (tests/test_gpu_engine.py). The
+// host knows each slot's finishing step (one token per step), so decode steps run back to back in
+// graph replays with no per-step synchronisation.
+int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, const uint32_t* lens,
+                   const detgpu_policy* pols, const uint64_t* seeds, uint32_t slots, uint32_t* const* tokens_out,
+                   float* const* logits_out, uint8_t* out_hash, bool v2, detgpu_stats* st) {
+    cudaStream_t s = E->stream;
+    int tmax = 1;
+    for (uint32_t i = 0; i < n_req; ++i) tmax = std::max<int>(tmax, static_cast<int>(pols[i].max_tokens));
+    if (int rc = ensure_outputs(E, static_cast<int>(slots), tmax)) return rc;
+    std::vector<int> init(slots, -1), zero(slots, 0);
+    ENG_CUDA(cudaMemcpyAsync(E->d_step, init.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_pos, init.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_status, zero.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaMemcpyAsync(E->d_tok, zero.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+    ENG_CUDA(cudaStreamSynchronize(s));
+    cudaGraphExec_t gx = nullptr;
+    if (tmax > 1)
+        if (int rc = get_graph(E, static_cast<int>(slots), &gx)) return rc;
+    std::vector<int> slot_req(slots, -1), slot_left(slots, 0);
+    uint32_t next = 0;
+    uint64_t nl = 0, decode_steps = 0;
+    Timer tall;
+    double prefill_ms = 0;
+    std::vector<int> ctok, cpos, creq, lin, lout, adm, pstep, pslot;
+    for (;;) {
+        // admit pending requests into free slots (max_tokens == 0 needs no GPU work)
+        adm.clear();
+        for (uint32_t sl = 0; sl < slots && next < n_req; ++sl) {
+            if (slot_req[sl] >= 0) continue;
+            while (next < n_req && pols[next].max_tokens == 0) {
+                if (out_hash) {
+                    if (v2) hash_canonical_v2_roots(nullptr, 0, nullptr, E->cfg.V, out_hash + 32 * size_t(next));
+                    else hash_canonical(nullptr, 0, nullptr, E->cfg.V, out_hash + 32 * size_t(next));
+                }
+                ++next;
+            }
+            if (next >= n_req) break;
+            slot_req[sl] = static_cast<int>(next++);
+            adm.push_back(static_cast<int>(sl));
+        }
+        if (!adm.empty()) {
+            Timer tp;
+            for (int sl : adm) {   // the slot's decode state before its first token is sampled
+                const int r = slot_req[sl];
+                uint64_t pr[4];
+                prng_seeded(seeds[r], pr);
+                const DevPolicy dp = to_dev_policy(pols[r]);
+                const int pos = static_cast<int>(lens[r]) - 1, z = 0;
+                ENG_CUDA(cudaMemcpyAsync(E->d_prng + 4 * size_t(sl), pr, sizeof(pr), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_pol + sl, &dp, sizeof(dp), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_pos + sl, &pos, sizeof(int), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_status + sl, &z, sizeof(int), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaStreamSynchronize(s));   // the host values above live on this frame
+                if (st) st->h2d_bytes += sizeof(pr) + sizeof(dp) + 2 * sizeof(int);
+            }
+            auto flush = [&]() -> int {
+                if (ctok.empty()) return DETGPU_OK;
+                const int nc = static_cast<int>(ctok.size());
+                ENG_CUDA(cudaMemcpyAsync(E->p_tok, ctok.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->p_pos, cpos.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->p_req, creq.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                const int nlast = static_cast<int>(lin.size());
+                if (nlast > 0) {
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_in, lin.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_out, lout.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                }
+                if (st) st->h2d_bytes += sizeof(int) * (3ull * nc + 2ull * nlast) + sizeof(uint32_t) * nc;
+                ENG_CUDA(forward(E, nc, E->p_tok, E->p_pos, E->p_req, false, nlast, &nl));
+                ENG_CUDA(cudaStreamSynchronize(s));
+                ctok.clear();
+                cpos.clear();
+                creq.clear();
+                lin.clear();
+                lout.clear();
+                return DETGPU_OK;
+            };
+            for (size_t j = 0; j < adm.size(); ++j) {   // prompts as prefill columns; h_last[j] = last position
+                const int r = slot_req[adm[j]];
+                for (uint32_t t = 0; t < lens[r]; ++t) {
+                    if (static_cast<int>(ctok.size()) == E->col_cap)
+                        if (int rc = flush()) return rc;
+                    if (t + 1 == lens[r]) {
+                        lin.push_back(static_cast<int>(ctok.size()));
+                        lout.push_back(static_cast<int>(j));
+                    }
+                    ctok.push_back(static_cast<int>(prompts[r][t]));
+                    cpos.push_back(static_cast<int>(t));
+                    creq.push_back(adm[j]);
+                }
+            }
+            if (int rc = flush()) return rc;
+            // first token of each admitted request: compact columns, trace step 0 of its slot
+            pstep.assign(adm.size(), 0);
+            pslot.assign(adm.begin(), adm.end());
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_in, pstep.data(), sizeof(int) * pstep.size(), cudaMemcpyHostToDevice, s));
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_out, pslot.data(), sizeof(int) * pslot.size(), cudaMemcpyHostToDevice, s));
+            ENG_CUDA(head_and_sample(E, E->h_last, static_cast<int>(adm.size()), &nl, false, E->p_last_in,
+                                     E->p_last_out, true));
+            ENG_CUDA(cudaStreamSynchronize(s));
+            for (int sl : adm) slot_left[sl] = static_cast<int>(pols[slot_req[sl]].max_tokens) - 1;
+            prefill_ms += tp.ms();
+        }
+        // collect finished slots, then run decode steps until the next one finishes
+        bool any = false;
+        for (uint32_t sl = 0; sl < slots; ++sl) {
+            if (slot_req[sl] < 0) continue;
+            if (slot_left[sl] == 0) {
+                const int r = slot_req[sl];
+                if (int rc = collect_slot(E, static_cast<int>(sl), pols[r].max_tokens, tokens_out ? tokens_out[r] : nullptr,
+                                          logits_out ? logits_out[r] : nullptr,
+                                          out_hash ? out_hash + 32 * size_t(r) : nullptr, v2, st))
+                    return rc;
+                slot_req[sl] = -1;
+            } else {
+                any = true;
+            }
+        }
+        if (!any) {
+            bool free_slot = false;
+            for (uint32_t sl = 0; sl < slots; ++sl) free_slot |= slot_req[sl] < 0;
+            if (next >= n_req) break;
+            if (free_slot) continue;
+        }
+        int k = INT32_MAX;
+        for (uint32_t sl = 0; sl < slots; ++sl)
+            if (slot_req[sl] >= 0) k = std::min(k, slot_left[sl]);
+        if (next < n_req) {
+            bool free_slot = false;
+            for (uint32_t sl = 0; sl < slots; ++sl) free_slot |= slot_req[sl] < 0;
+            if (free_slot) k = std::min(k, 0);   // admit first
+        }
+        for (int t = 0; t < k; ++t) ENG_CUDA(cudaGraphLaunch(gx, s));
+        decode_steps += static_cast<uint64_t>(std::max(k, 0));
+        for (uint32_t sl = 0; sl < slots; ++sl)
+            if (slot_req[sl] >= 0) slot_left[sl] -= k;
+        ENG_CUDA(cudaStreamSynchronize(s));
+    }
+    if (st) {
+        st->prefill_ms += static_cast<float>(prefill_ms);
+        st->decode_ms += static_cast<float>(tall.ms() - prefill_ms);
+        st->decode_steps += decode_steps;
+        st->kernel_launches += nl + decode_steps * E->launches_per_step;
     }
     return DETGPU_OK;
 }
@@ -923,6 +1086,14 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
         return toy_generate(E->toyw, n_req, prompts, prompt_lens, policies, seeds, batch_size, tokens_out, logits_out,
                             out_hash, flags, stats, E->stream, &E->err);
     const uint32_t group = std::min(batch_size, E->max_batch);
+    if ((flags & DETGPU_F_CONTINUOUS) && !(flags & DETGPU_F_DEVICE_ONLY)) {
+        if (int rc = run_continuous(E, n_req, prompts, prompt_lens, policies, seeds, group, tokens_out, logits_out,
+                                    out_hash, (flags & DETGPU_F_RECEIPT_V2) != 0, stats))
+            return rc;
+        if (stats)
+            for (uint32_t i = 0; i < n_req; ++i) stats->tokens += policies[i].max_tokens;
+        return DETGPU_OK;
+    }
     Timer total;
     for (uint32_t base = 0; base < n_req; base += group) {
         const uint32_t n = std::min(group, n_req - base);

@@ -613,16 +613,17 @@ __device__ __forceinline__ void sample_tail(const SampleParams& sp, SampleSmem& 
     }
 
     if (tid == 0) {
-        sp.token_out[r] = static_cast<uint32_t>(token);
+        const int sr = sp.state_by_slot ? slot : r;   // where the decode state of this row lives
+        sp.token_out[sr] = static_cast<uint32_t>(token);
         if (err != DETGPU_OK) sp.status[slot] = err;
         if (sp.tokens_hist != nullptr) sp.tokens_hist[static_cast<int64_t>(slot) * sp.tcap + step] = token;
         if (sp.col_step_mut != nullptr) {
             if (err != DETGPU_OK || step + 1 >= pol.max_tokens) {
-                sp.col_step_mut[r] = -1;
-                sp.col_pos[r] = -1;
+                sp.col_step_mut[sr] = -1;
+                sp.col_pos[sr] = -1;
             } else {
-                sp.col_step_mut[r] = step + 1;
-                sp.col_pos[r] = sp.col_pos[r] + 1;
+                sp.col_step_mut[sr] = step + 1;
+                sp.col_pos[sr] = sp.col_pos[sr] + 1;
             }
         }
     }
@@ -641,10 +642,11 @@ __device__ __forceinline__ float sample_draw(const SampleParams& sp, int slot) {
 
 __device__ __forceinline__ void sample_fail_nonfinite(const SampleParams& sp, int r, int slot) {
     sp.status[slot] = DETGPU_ENONFINITE;
-    sp.token_out[r] = 0;
+    const int sr = sp.state_by_slot ? slot : r;
+    sp.token_out[sr] = 0;
     if (sp.col_step_mut != nullptr) {
-        sp.col_step_mut[r] = -1;
-        sp.col_pos[r] = -1;
+        sp.col_step_mut[sr] = -1;
+        sp.col_pos[sr] = -1;
     }
 }
 

@@ -93,6 +93,7 @@ struct SampleParams {
     int tcap;
     int* col_pos;
     int* col_step_mut;
+    int state_by_slot;          // token_out / col_pos / col_step_mut indexed by slot (else by row)
     // small batches (rows <= kSampleMultiMaxRows, nullable): the row is split over several CTAs
     float* blk_ws;              // [rows][kSampleMaxBlocks][4] block max / non-finite / subtree sum
     int* tickets;               // [rows], zero-initialised; reset by the last block

@@ -259,9 +259,11 @@ class Engine:
         L.check(L.lib.detgpu_set_option(self.h, name.encode(), int(value)), self.h)
 
     def generate(self, prompts, policies, seeds, batch_size: Optional[int] = None, want_logits: bool = True,
-                 want_hash: bool = True, device_only: bool = False, receipt_v2: bool = False):
+                 want_hash: bool = True, device_only: bool = False, receipt_v2: bool = False,
+                 continuous: bool = False):
         """Returns (tokens list[np.uint32], logits list[np.float32 [T,V]] or None, hashes list[bytes]).
-        receipt_v2: hashes are the v2 digest (per-step Merkle roots on the GPU)."""
+        receipt_v2: hashes are the v2 digest (per-step Merkle roots on the GPU).
+        continuous: batch_size decode slots stay busy, requests admitted as slots free (same bytes)."""
         n = len(prompts)
         pr = [np.ascontiguousarray(p, dtype=np.uint32) for p in prompts]
         pr_ptrs = (C.POINTER(C.c_uint32) * n)(*[p.ctypes.data_as(C.POINTER(C.c_uint32)) for p in pr])
@@ -280,7 +282,8 @@ class Engine:
         stats = L.Stats()
         rc = L.lib.detgpu_generate(self.h, n, pr_ptrs, lens, pols, sd, batch_size or self.max_batch, tok_ptrs, lg_ptrs,
                                    hashes.ctypes.data_as(C.POINTER(C.c_uint8)) if hashes is not None else None,
-                                   (L.F_DEVICE_ONLY if device_only else 0) | (L.F_RECEIPT_V2 if receipt_v2 else 0),
+                                   (L.F_DEVICE_ONLY if device_only else 0) | (L.F_RECEIPT_V2 if receipt_v2 else 0)
+                                   | (L.F_CONTINUOUS if continuous else 0),
                                    C.byref(stats))
         L.check(rc, self.h)
         self.last_stats = stats

@@ -167,3 +167,32 @@ def test_tiny_max_tokens_zero_and_errors(tiny):
 
     with pytest.raises(ValueError, match="batch_size must be positive"):
         infer_batch([ExecutionTuple("llama-tiny:model-a", decode_policy=DecodePolicy.greedy(2), prompt=[1])], 0)
+
+
+@pytest.mark.parametrize("receipt_v2", [False, True])
+def test_continuous_batching_is_bit_identical(receipt_v2):
+    """DETGPU_F_CONTINUOUS: requests admitted into free decode slots between steps,
+    prefilled while other slots decode; every request's tokens, logits and out_hash equal the
+    static-group path's and the one-at-a-time path's."""
+    import numpy as np
+
+    from paper_2602_00182_b200 import replicas
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    eng = Engine("llama-tiny:serve", "b200", max_batch=16, max_context=160)
+    V = eng.vocab
+    n = 14
+    prompts = [replicas.synthetic_prompt(100 + i, 3 + (i * 7) % 40, V) for i in range(n)]
+    kinds = [DecodePolicy.greedy, lambda t: DecodePolicy.nucleus(0.9, t), lambda t: DecodePolicy.top_k(5, t)]
+    lengths = [1, 9, 0, 17, 4, 30, 2, 11, 25, 1, 6, 14, 3, 20]
+    pols = [kinds[i % 3](lengths[i]) for i in range(n)]
+    seeds = [replicas.request_seed(i) for i in range(n)]
+    ref_t, ref_l, ref_h = eng.generate(prompts, pols, seeds, batch_size=n, receipt_v2=receipt_v2)
+    for slots in (3, 5, 1):
+        t, l, h = eng.generate(prompts, pols, seeds, batch_size=slots, receipt_v2=receipt_v2, continuous=True)
+        assert h == ref_h, slots
+        for i in range(n):
+            assert np.array_equal(t[i], ref_t[i]) and np.array_equal(l[i].view(np.uint32), ref_l[i].view(np.uint32))
+    one = [eng.generate([prompts[i]], [pols[i]], [seeds[i]], receipt_v2=receipt_v2)[2][0] for i in (0, 3, 5, 8)]
+    assert one == [ref_h[i] for i in (0, 3, 5, 8)]
+    eng.close()
