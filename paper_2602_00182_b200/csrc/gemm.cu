@@ -684,15 +684,17 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     if (S > 1 && !push) {
         cluster_sync_all();   // partial tiles of all segments visible cluster-wide
         if (tracing && threadIdx.x == 128) s_tm[5] = globaltimer_ns();   // cluster exchange ready
-        if (warp >= 4) {
-            const int rl = (warp - 4) * 32 + lane;
+        {
+            // all eight warps: the partials come from shared memory, not TMEM, so any warp can take
+            // any rows; warp group wg = warp / 4 takes every other round of column quads
+            const int rl = (warp & 3) * 32 + lane, wg = warp >> 2;
             const ExpTab tab = exp_tab_lane();
             const uint32_t pbase = smem_u32(smem);
             // CTA `seg` finalises column quads seg, seg+S, ...; QB quads per round trip so that all
             // their DSMEM loads are in flight together.
             constexpr int QB = NSUB <= 2 ? 1 : 2;
             const int nq = ncols <= 8 ? 0 : (ncols + 3) >> 2;
-            for (int cl = seg; ncols <= 8 && cl < ncols; cl += S) {   // decode: one column per CTA
+            for (int cl = seg; warp >= 4 && ncols <= 8 && cl < ncols; cl += S) {   // one column per CTA
                 float v[8];
 #pragma unroll
                 for (int s = 0; s < 8; ++s)
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 const float xn = epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
                 if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, warp - 4, lane, s_red);
             }
-            for (int q0 = seg; q0 < nq; q0 += QB * S) {
+            for (int q0 = seg + wg * QB * S; q0 < nq; q0 += 2 * QB * S) {
                 float4 v[QB][8];
 #pragma unroll
                 for (int u = 0; u < QB; ++u) {
@@ -726,8 +728,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
 #pragma unroll
                             for (int s = 0; s < 8; ++s)
                                 t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
-                            const float xn = epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(t), tab);
-                            if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, warp - 4, lane, s_red);
+                            epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(t), tab);   // ss_out: <= 8 cols
                         }
                     }
                 }
