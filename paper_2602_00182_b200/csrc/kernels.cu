@@ -100,6 +100,31 @@ __device__ float block_tree_sum_1024_fm(int n, Fetch fetch, Map map, float* s_ti
 }
 
 // ------------------------------------------------------------------ RMSNorm
+// E contiguous bf16 <-> f32 per thread, 16-byte vectors when E % 8 == 0 (a warp then touches whole
+// sectors instead of one 2-byte element per sector per instruction)
+template <int E>
+__device__ __forceinline__ void load_bf16_row(const __nv_bfloat16* __restrict__ src, float (&v)[E]) {
+    if constexpr (E % 8 == 0) {
+#pragma unroll
+        for (int j = 0; j < E; j += 8) {
+            const uint4 w = *reinterpret_cast<const uint4*>(src + j);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[j + 2 * k] = __uint_as_float(ws[k] << 16);
+                v[j + 2 * k + 1] = __uint_as_float(ws[k] & 0xffff0000u);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = bf2f(src[j]);
+    }
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    return static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(a))) |
+           (static_cast<uint32_t>(__bfloat16_as_ushort(f2bf(b))) << 16);
+}
+
 // y_i = bf16((x_i * rstd) * gamma_i), rstd = 1 / sqrt(tree(x*x)/d + eps)
 template <int E>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x_in, float* __restrict__ x_out,
@@ -117,12 +142,15 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
     float v[E];
     if (embed != nullptr) {
         const int tok = col_token[col];
-        const __nv_bfloat16* src = embed + static_cast<int64_t>(tok) * d + base;
-#pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = bf2f(src[j]);
+        load_bf16_row<E>(embed + static_cast<int64_t>(tok) * d + base, v);
         float* dst = x_out + static_cast<int64_t>(col) * d + base;
+        if constexpr (E % 4 == 0) {
 #pragma unroll
-        for (int j = 0; j < E; ++j) dst[j] = v[j];
+            for (int j = 0; j < E; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < E; ++j) dst[j] = v[j];
+        }
         if (ss_out != nullptr) {
             // per-128-element partial sums of squares of the new residual row (fused-norm decode):
             // warp w reduces tiles w, w+8, ... with 4 contiguous elements per lane + the butterfly
@@ -163,8 +191,22 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
     const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
     const int orow = out_index != nullptr ? out_index[col] : col;
     __nv_bfloat16* o = out + static_cast<int64_t>(orow) * d + base;
+    float g[E];
+    load_bf16_row<E>(gamma + base, g);
+    if constexpr (E % 8 == 0) {
 #pragma unroll
-    for (int j = 0; j < E; ++j) o[j] = f2bf(__fmul_rn(__fmul_rn(v[j], rstd), bf2f(gamma[base + j])));
+        for (int j = 0; j < E; j += 8) {
+            uint4 w;
+            w.x = pack_bf16x2(__fmul_rn(__fmul_rn(v[j], rstd), g[j]), __fmul_rn(__fmul_rn(v[j + 1], rstd), g[j + 1]));
+            w.y = pack_bf16x2(__fmul_rn(__fmul_rn(v[j + 2], rstd), g[j + 2]), __fmul_rn(__fmul_rn(v[j + 3], rstd), g[j + 3]));
+            w.z = pack_bf16x2(__fmul_rn(__fmul_rn(v[j + 4], rstd), g[j + 4]), __fmul_rn(__fmul_rn(v[j + 5], rstd), g[j + 5]));
+            w.w = pack_bf16x2(__fmul_rn(__fmul_rn(v[j + 6], rstd), g[j + 6]), __fmul_rn(__fmul_rn(v[j + 7], rstd), g[j + 7]));
+            *reinterpret_cast<uint4*>(o + j) = w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) o[j] = f2bf(__fmul_rn(__fmul_rn(v[j], rstd), g[j]));
+    }
 }
 
 // ------------------------------------------------------------------ misc test kernels

@@ -34,15 +34,16 @@ ap.add_argument("--layers", type=int, default=3)
 ap.add_argument("--l2pf", type=int, default=None)
 ap.add_argument("--json", default=None)
 ap.add_argument("--raw", default=None, help="save the last step's records (.npy)")
+ap.add_argument("--cap", type=int, default=1 << 20, help="trace buffer capacity (records)")
 a = ap.parse_args()
 
 eng = Engine("llama3-8b:bench", "b200", max_batch=max(a.batch, 1), max_context=768)
 if a.l2pf is not None:
     eng.set_option("l2pf_mask", a.l2pf)
-eng.set_option("trace", 1 << 20)
+eng.set_option("trace", a.cap)
 ms = C.c_float()
 L.check(L.lib.detgpu_profile_graph(eng.h, a.batch, a.ctx, 0, 1, C.byref(ms)), eng.h)   # 3 warm-up + 1
-buf = np.zeros(1 << 20, dtype=REC)
+buf = np.zeros(a.cap, dtype=REC)
 n = C.c_uint32()
 L.check(L.lib.detgpu_trace_read(eng.h, buf.ctypes.data, len(buf), C.byref(n)), eng.h)
 r = buf[: n.value]
