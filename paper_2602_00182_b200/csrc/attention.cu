@@ -11,6 +11,7 @@
 // queries see exactly the same arithmetic as decode steps.
 #include <cfloat>
 
+#include "common.h"
 #include "detmath.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         }
         leave();
     }
-    if (nch == 1 && !a.partials_only) {
+    if (nch == 1) {
         // single chunk: the combine weight is exp(0) == 1 exactly
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
@@ -344,7 +345,6 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         ws[tid * (HD + 4)] = sM[tid];
         ws[tid * (HD + 4) + 1] = sL[tid];
     }
-    if (a.partials_only) return;   // the o-projection GEMM combines the chunks (gemm.cu attn_b_setup)
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -379,14 +379,15 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
 template <int HD, int G, bool CL>
 cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
     constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_devs{0};
+    int dev = 0;
+    if (attrs_needed(attr_devs, &dev)) {
         cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
         if (e == cudaSuccess && CL)
             e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attrs_done(attr_devs, dev);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.max_chunks, a.hkv, a.ncols);
@@ -410,7 +411,7 @@ cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
 // fit the leader's K/V buffer; the workspace/ticket combine otherwise.
 template <int HD, int G>
 cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    const bool cl = !a.partials_only && a.max_chunks <= kMaxClusterChunks &&
+    const bool cl = a.max_chunks <= kMaxClusterChunks &&
                     static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 <= 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
     return cl ? launch_hgc<HD, G, true>(a, stream, pdl) : launch_hgc<HD, G, false>(a, stream, pdl);
 }

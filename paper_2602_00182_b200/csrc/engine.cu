@@ -110,9 +110,6 @@ struct Engine {
     // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
     // Default: the o-projection warms the first 16 MB of gate/up (tools/l2pf_scan.py).
     unsigned l2pf_mask = 2;
-    // decode: combine the attention chunks in the o-projection's B setup (1) instead of inside the
-    // attention kernel's cluster (0, default)
-    bool attn_fuse = false;
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
     int max_nsub = 0;     // GemmParams::max_nsub
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
@@ -321,13 +318,6 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     // Decode with <= 8 columns: RMSNorm is fused into the consuming GEMMs (QKV, gate/up, lm_head),
     // which build their B operand from the f32 residual stream; bits are identical.
     const bool fuse = final_all && ncols <= 8;
-    // the o-projection combines the attention chunks itself when its K-segments fall on heads
-    bool fuse_attn = fuse && E->attn_fuse && E->max_chunks <= 16;
-    {
-        const int S = gemm_ksplit(d, qd), nkb = qd / 64;
-        for (int sg = 0; sg <= S && fuse_attn; ++sg)
-            if (((sg * nkb / S) * 64) % c.hd != 0 || ((nkb * 64 / S) / c.hd) > 8) fuse_attn = false;
-    }
     e = launch_embed(E->embed, tok, E->x, fuse ? E->norm_ss : nullptr, E->layers[0].attn_norm, E->h, ncols, d, c.eps, s,
                      pdl);
     if (e != cudaSuccess) return e;
@@ -386,7 +376,6 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_pages = E->pages_per_slot;
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
-        a.partials_only = fuse_attn ? 1 : 0;   // the o-projection GEMM combines the chunks
         a.trace = E->trace_buf;
         a.trace_tag = kProfAttn;
         if (pf & 1u) {
@@ -403,15 +392,6 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         if (fuse) {
             go.ss_out = E->norm_ss;
             go.ss_tiles = d / 128;
-        }
-        if (fuse_attn) {
-            go.attn_ws = E->attn_ws;
-            go.attn_pos = pos;
-            go.attn_hkv = c.hkv;
-            go.attn_G = c.hq / c.hkv;
-            go.attn_hd = c.hd;
-            go.attn_max_chunks = E->max_chunks;
-            go.attn_chunk = kAttnChunk;
         }
         if (pf & 2u) {
             go.l2pf = Ly.wgu;
@@ -1201,7 +1181,6 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     if (std::strcmp(name, "l2pf_mask") == 0) E->l2pf_mask = static_cast<unsigned>(value);
     else if (std::strcmp(name, "l2pf_cap_mb") == 0) E->l2pf_cap = value << 20;
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
-    else if (std::strcmp(name, "attn_fuse") == 0) E->attn_fuse = value != 0;
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "trace") == 0) {

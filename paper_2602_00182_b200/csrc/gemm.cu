@@ -10,6 +10,7 @@
 // split across CTAs.
 #include <cfloat>
 
+#include "common.h"
 #include "gemm.cuh"
 #include "detmath.cuh"
 #include "ptx.cuh"
@@ -332,112 +333,6 @@ __device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready,
     }
 }
 
-// O-projection input from attention chunk partials ws[col][kvh][chunk][g][4 + hd] = (m, l, -, -, o[hd]).
-// Phase 1 (per column and head): M = max_c m_c, a_c = exp(m_c - M), L = fma chain of l_c a_c in
-// chunk order; all (m, l) loads and the positions in one round trip, the chains interleaved.
-// Phase 2: O_d = fma chain of o_cd a_c in chunk order, B = bf16(O_d / L), k-block-major with
-// progressive release as in norm_b_setup.
-__device__ void attn_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready, int kb0, int nkb, int col0,
-                             int ncols, int ew, int lane, ExpTab tab, uint64_t* tm) {
-    auto mark = [&](int i) {
-        if (tm != nullptr && ew == 0 && lane == 0) tm[i] = globaltimer_ns();
-    };
-    constexpr int kMaxH = 8, kMaxC = 16, PB = 16;   // PB: (column, head) pairs per warp
-    __shared__ float s_al[8][kMaxH][kMaxC];   // combine weights a_c per (column, head)
-    __shared__ float s_L[8][kMaxH];
-    __shared__ int s_nch[8];
-    const int hd = p.attn_hd, G = p.attn_G, hkv = p.attn_hkv, mc = p.attn_max_chunks;
-    const int h0 = kb0 * BK / hd;                            // first head of this K-segment
-    const int nh = (nkb * BK + hd - 1) / hd;
-    const int npairs = ncols * nh;
-    auto wsp = [&](int col, int h, int ch) {
-        return p.attn_ws + ((static_cast<int64_t>(col0 + col) * hkv + h / G) * mc + ch) * G * (hd + 4) +
-               (h % G) * (hd + 4);
-    };
-    const int posl = lane < ncols ? p.attn_pos[col0 + lane] : -1;
-    float m[PB], l[PB], al[PB], L[PB];
-    int nchj[PB];
-#pragma unroll
-    for (int j = 0; j < PB; ++j) {   // chunk slots beyond a column's count are masked below
-        const int q = ew + 4 * j;
-        m[j] = -FLT_MAX;
-        l[j] = 0.0f;
-        if (q < npairs && lane < mc) {
-            const float* w = wsp(q / nh, h0 + q % nh, lane);
-            m[j] = __ldcg(w);
-            l[j] = __ldcg(w + 1);
-        }
-    }
-    int maxnch = 0;
-    mark(9);
-#pragma unroll
-    for (int j = 0; j < PB; ++j) {
-        const int q = ew + 4 * j;
-        nchj[j] = 0;
-        al[j] = 0.0f;
-        L[j] = 0.0f;
-        if (q < npairs) {   // warp-uniform
-            const int cc = q / nh, hl = q % nh;
-            const int pos = __shfl_sync(0xffffffffu, posl, cc);
-            const int nch = pos < 0 ? 0 : (pos + p.attn_chunk) / p.attn_chunk;
-            nchj[j] = nch;
-            maxnch = max(maxnch, nch);
-            const float mj = lane < nch ? m[j] : -FLT_MAX;
-            const float M = warp_max(mj);
-            al[j] = det_expf_shfl(lane < nch ? __fsub_rn(mj, M) : 0.0f, tab);   // all lanes
-            if (lane < nch) s_al[cc][hl][lane] = al[j];
-        }
-    }
-    mark(10);
-    for (int ch = 0; ch < maxnch; ++ch) {
-#pragma unroll
-        for (int j = 0; j < PB; ++j) {
-            const float lc = __shfl_sync(0xffffffffu, l[j], ch), ac = __shfl_sync(0xffffffffu, al[j], ch);
-            if (ch < nchj[j]) L[j] = __fmaf_rn(lc, ac, L[j]);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < PB; ++j) {
-        const int q = ew + 4 * j;
-        if (q < npairs && lane == 0) s_L[q / nh][q % nh] = L[j];
-    }
-    if (ew == 0 && lane < ncols) s_nch[lane] = posl < 0 ? 0 : (posl + p.attn_chunk) / p.attn_chunk;
-    mark(11);
-    epi_bar();
-    mark(12);
-    const int t = ew * 32 + lane;
-    const int per_kb = ncols * 16, total = nkb * per_kb;
-    int released = 0;
-    for (int q0 = 0; q0 < total; q0 += 128) {
-        const int q = q0 + t;
-        if (q < total) {
-            const int i = q / per_kb, rem = q % per_kb, c = rem >> 4, kq = (rem & 15) * 4;
-            const int nch = s_nch[c];
-            const int k = (kb0 + i) * BK + kq;   // input feature = head * hd + d
-            const int h = k / hd, hl = h - h0, dd = k % hd;
-            float4 ov[kMaxC];
-#pragma unroll
-            for (int ch = 0; ch < kMaxC; ++ch)   // all loads in flight before the chain
-                if (ch < nch) ov[ch] = __ldcg(reinterpret_cast<const float4*>(wsp(c, h, ch) + 4 + dd));
-            float O0 = 0.0f, O1 = 0.0f, O2 = 0.0f, O3 = 0.0f;
-#pragma unroll
-            for (int ch = 0; ch < kMaxC; ++ch) {
-                if (ch < nch) {
-                    const float a = s_al[c][hl][ch];
-                    O0 = __fmaf_rn(ov[ch].x, a, O0);
-                    O1 = __fmaf_rn(ov[ch].y, a, O1);
-                    O2 = __fmaf_rn(ov[ch].z, a, O2);
-                    O3 = __fmaf_rn(ov[ch].w, a, O3);
-                }
-            }
-            const float Lc = s_L[c][hl];
-            put_b(bc, i, c, kq, __fdiv_rn(O0, Lc), __fdiv_rn(O1, Lc), __fdiv_rn(O2, Lc), __fdiv_rn(O3, Lc));
-        }
-        if (q0 == 0) mark(13);
-        release_b_range(bready, released, q0 + 128 >= total ? nkb : (q0 + 128) / per_kb);
-    }
-}
-
 // Grid (S, n_out/128, column groups), cluster (S,1,1): the S CTAs of a cluster own the same 128
 // weight rows and columns and the fixed K-segments [s*nkb/S, (s+1)*nkb/S) of the reduction. Each
 // runs its segment as one tcgen05 accumulation chain in TMEM; the S partial tiles are exchanged
@@ -480,8 +375,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     // Fused RMSNorm (decode, <= 8 columns): the B operand is produced in shared memory by the
     // epilogue warps from the f32 residual stream instead of being loaded by TMA from a separately
     // normalised bf16 copy; bits are identical to rmsnorm_kernel + TMA.
-    const int bmode = p.norm_x != nullptr ? 1 : (p.attn_ws != nullptr ? 2 : 0);
-    const bool fused = bmode != 0;
+    const bool fused = p.norm_x != nullptr;
     uint8_t* bc = sB;   // fused B buffer: 1 KB per k-block (see norm_b_setup)
     // Decode (<= 8 columns): column cl is finalised by CTA cl % S; every other segment pushes its
     // partial of that column straight into the owner's receive buffer (st.async + mbarrier), so the
@@ -536,7 +430,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                                  (static_cast<int64_t>(tile) * nkb_all + kb0 + pre) * A_BYTES,
                              static_cast<uint32_t>(npf) * A_BYTES);
     }
-    if (bmode == 1 && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
+    if (fused && warp >= 4)   // RMSNorm gamma of this K-segment (a weight): warm L2 before the wait
         for (int i = threadIdx.x - 128; i < nkb; i += 128) prefetch_l2(p.norm_gamma + (kb0 + i) * BK);
     // Every kernel waits for its predecessor before triggering its dependents, so when a kernel
     // starts, all kernels before its predecessor have completed (attention relies on this).
@@ -605,10 +499,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         const int ew = warp - 4;       // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
         const int rl = ew * 32 + lane;
         const ExpTab tab = exp_tab_lane();
-        if (fused) {
-            if (bmode == 1) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
-            else attn_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane, tab, tracing ? s_tm : nullptr);
-        }
+        if (fused) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
         if (tracing && threadIdx.x == 128) s_tm[2] = globaltimer_ns();   // B operand built (fused)
         EpiPre pre{0.0f, 0.0f, -1, 0};   // the first owned column's epilogue operands (decode)
         if (push && seg < ncols) pre = epilogue_preload(p, m0 + rl, col0 + seg);
@@ -768,11 +659,12 @@ template <int NSUB>
 cudaError_t launch_nsub(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p, cudaStream_t stream,
                         bool pdl) {
     using C = Cfg<NSUB>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_devs{0};
+    int dev = 0;
+    if (attrs_needed(attr_devs, &dev)) {
         cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attrs_done(attr_devs, dev);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.ksplit, (p.ncols + NSUB * SUB_N - 1) / (NSUB * SUB_N), p.n_out / BM);
@@ -845,13 +737,7 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     if (p.ksplit <= 0) p.ksplit = gemm_ksplit(p.n_out, p.k);
     if (p.ksplit > 8 || p.ksplit > p.k / BK) return cudaErrorInvalidValue;
     const int seg_kb = (p.k / BK + p.ksplit - 1) / p.ksplit;
-    if ((p.norm_x != nullptr || p.attn_ws != nullptr) && (p.ncols > 8 || seg_kb > 35)) return cudaErrorInvalidValue;
-    if (p.attn_ws != nullptr) {
-        if (p.attn_max_chunks > 16 || p.attn_hd % 64 != 0 || (seg_kb * BK) / p.attn_hd > 8 || p.norm_x != nullptr)
-            return cudaErrorInvalidValue;
-        for (int sg = 0; sg <= p.ksplit; ++sg)   // every K-segment boundary must fall on a head boundary
-            if (((sg * (p.k / BK) / p.ksplit) * BK) % p.attn_hd != 0) return cudaErrorInvalidValue;
-    }
+    if (p.norm_x != nullptr && (p.ncols > 8 || seg_kb > 35)) return cudaErrorInvalidValue;
     if (p.norm_x != nullptr && (p.ncols > 8 || p.norm_ss == nullptr || p.k != p.norm_d || (p.norm_d & (p.norm_d - 1)) != 0 ||
                                 p.norm_d < 256 || p.norm_d > 4096))
         return cudaErrorInvalidValue;

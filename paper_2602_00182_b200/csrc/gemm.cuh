@@ -57,11 +57,6 @@ struct GemmParams {
     const __nv_bfloat16* norm_gamma;
     int norm_d;
     float norm_eps;
-    // fused attention combine of the B operand (o-projection, decode, <= 8 columns): X[col][h*hd+d]
-    // = bf16(O/L) of the attention chunk partials (attention.cu partials_only), combined in chunk order
-    const float* attn_ws;      // or nullptr
-    const int* attn_pos;       // query position per column (<0 inactive)
-    int attn_hkv, attn_G, attn_hd, attn_max_chunks, attn_chunk;
     // kEpiAddF32 in fused decode: emit the next RMSNorm's per-tile sums of squares of the result
     float* ss_out;             // [ncols][ss_tiles] or nullptr
     int ss_tiles;              // n_out / 128
