@@ -196,3 +196,18 @@ def test_continuous_batching_is_bit_identical(receipt_v2):
     one = [eng.generate([prompts[i]], [pols[i]], [seeds[i]], receipt_v2=receipt_v2)[2][0] for i in (0, 3, 5, 8)]
     assert one == [ref_h[i] for i in (0, 3, 5, 8)]
     eng.close()
+
+
+def test_tiny_context_beyond_cluster_path(tiny_oracle):
+    """max_context 1536 (24 attention chunks > the 16-CTA cluster limit): the workspace + ticket
+    combine path, prefill and decode, bit-exact with the oracle."""
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    eng = Engine("llama-tiny:model-a", "b200", max_batch=2, max_context=1536)
+    prompt = _prompt(21, 1100, eng.vocab)
+    toks, logits, h = eng.generate([prompt], [DecodePolicy.greedy(6)], [0])
+    ot, ol = tiny_oracle.generate(prompt, max_tokens=6)
+    assert toks[0].tolist() == ot.tolist()
+    assert (logits[0].view(np.uint32) == ol.view(np.uint32)).all()
+    assert h[0] == O.out_hash(ot, ol)
+    eng.close()
