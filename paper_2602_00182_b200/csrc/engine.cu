@@ -13,6 +13,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <future>
 #include <thread>
 #include <vector>
 
@@ -686,7 +687,7 @@ int run_group(Engine* E, uint32_t n, const uint32_t* const* prompts, const uint3
 // hashing piece k while k+1 lands) and out_hash (v1: SHA-256 of the canonical bytes; v2: the
 // per-step Merkle roots computed on the GPU).
 int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* logits_out, uint8_t* out_hash, bool v2,
-                 detgpu_stats* st) {
+                 detgpu_stats* st, std::vector<std::future<void>>* hashers = nullptr) {
     const int V = E->cfg.V;
     cudaStream_t s = E->stream;
     int status = 0;
@@ -725,6 +726,27 @@ int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* l
         hash_ms += th.ms();
     }
     const bool want_hash = out_hash != nullptr && !v2;
+    if (want_hash && hashers != nullptr && T > 0) {
+        // continuous batching: copy the slot's trace out and hash it on a worker thread, so that
+        // the v1 SHA-256 (sequential, ~71 ms per 8B request) does not stall the decode loop
+        std::shared_ptr<std::vector<float>> own;
+        float* dst = logits_out;
+        if (dst == nullptr) {
+            own = std::make_shared<std::vector<float>>(size_t(T) * V);
+            dst = own->data();
+        }
+        Timer tw;
+        ENG_CUDA(cudaMemcpy(dst, E->trace + size_t(slot) * E->slot_stride, sizeof(float) * size_t(T) * V,
+                            cudaMemcpyDeviceToHost));
+        copy_ms += tw.ms();
+        if (st) st->d2h_bytes += 4 * size_t(T) * V;
+        auto tk = std::make_shared<std::vector<uint32_t>>(toks.begin(), toks.begin() + T);
+        hashers->push_back(std::async(std::launch::async, [tk, own, dst, T, V, out_hash]() {
+            hash_canonical(tk->data(), T, dst, static_cast<uint32_t>(V), out_hash);
+        }));
+        if (st) st->d2h_ms += static_cast<float>(copy_ms);
+        return DETGPU_OK;
+    }
     if (logits_out != nullptr || want_hash) {
         const size_t piece = E->pinned_floats;
         Sha256 sha;
@@ -782,14 +804,17 @@ int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* l
 
 int collect_group(Engine* E, uint32_t n, const detgpu_policy* pols, uint32_t* const* tokens_out,
                   float* const* logits_out, uint8_t* out_hash, bool v2, detgpu_stats* st) {
-    for (uint32_t i = 0; i < n; ++i) {
+    // several requests: hash them on worker threads (one request: the streamed, copy-overlapped hash)
+    std::vector<std::future<void>> hashers;
+    int rc = DETGPU_OK;
+    for (uint32_t i = 0; i < n && rc == DETGPU_OK; ++i) {
         if (pols[i].max_tokens == 0) continue;   // handled by the caller (empty canonical output)
-        if (int rc = collect_slot(E, static_cast<int>(i), pols[i].max_tokens, tokens_out ? tokens_out[i] : nullptr,
-                                  logits_out ? logits_out[i] : nullptr, out_hash ? out_hash + 32 * size_t(i) : nullptr,
-                                  v2, st))
-            return rc;
+        rc = collect_slot(E, static_cast<int>(i), pols[i].max_tokens, tokens_out ? tokens_out[i] : nullptr,
+                          logits_out ? logits_out[i] : nullptr, out_hash ? out_hash + 32 * size_t(i) : nullptr, v2, st,
+                          n > 1 ? &hashers : nullptr);
     }
-    return DETGPU_OK;
+    for (auto& f : hashers) f.wait();
+    return rc;
 }
 
 // Continuous batching: `slots` decode slots stay busy; a request is admitted into a
@@ -821,6 +846,14 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
     Timer tall;
     double prefill_ms = 0;
     std::vector<int> ctok, cpos, creq, lin, lout, adm, pstep, pslot;
+    std::vector<std::future<void>> hashers;   // v1 receipts hashed off the decode loop
+    struct Join {
+        std::vector<std::future<void>>& h;
+        ~Join() {
+            for (auto& f : h)
+                if (f.valid()) f.wait();
+        }
+    } join{hashers};
     for (;;) {
         // admit pending requests into free slots (max_tokens == 0 needs no GPU work)
         adm.clear();
@@ -907,7 +940,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
                 const int r = slot_req[sl];
                 if (int rc = collect_slot(E, static_cast<int>(sl), pols[r].max_tokens, tokens_out ? tokens_out[r] : nullptr,
                                           logits_out ? logits_out[r] : nullptr,
-                                          out_hash ? out_hash + 32 * size_t(r) : nullptr, v2, st))
+                                          out_hash ? out_hash + 32 * size_t(r) : nullptr, v2, st, &hashers))
                     return rc;
                 slot_req[sl] = -1;
             } else {
