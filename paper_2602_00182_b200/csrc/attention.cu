@@ -156,6 +156,45 @@ __device__ __forceinline__ void chunk_pv(const __nv_bfloat16* sV, const float* s
     }
 }
 
+// The workspace combine of one (head, d) chain over nch chunk partials in chunk order:
+// M = max m_c, a_c = exp(m_c - M), out = bf16(fma-chain(o_c a_c) / fma-chain(l_c a_c)). Loads are
+// issued eight chunks at a time before their arithmetic (one L2 round trip per eight chunks).
+// Warp-uniform nch (det_expf_shfl).
+__device__ __forceinline__ __nv_bfloat16 combine_ws_chain(const float* base, int64_t cstride, int nch, int d,
+                                                          ExpTab tab) {
+    constexpr int B = 8;
+    float M = -FLT_MAX;
+    for (int c0 = 0; c0 < nch; c0 += B) {
+        float m[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) m[u] = c0 + u < nch ? __ldcg(base + (c0 + u) * cstride) : -FLT_MAX;
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (c0 + u < nch) M = fmaxf(M, m[u]);
+    }
+    float L = 0.0f, O = 0.0f;
+    for (int c0 = 0; c0 < nch; c0 += B) {
+        float m[B], l[B], o[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const float* w = base + (c0 + u) * cstride;
+            const bool ok = c0 + u < nch;
+            m[u] = ok ? __ldcg(w) : 0.0f;
+            l[u] = ok ? __ldcg(w + 1) : 0.0f;
+            o[u] = ok ? __ldcg(w + 4 + d) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const float al = det_expf_shfl(c0 + u < nch ? __fsub_rn(m[u], M) : 0.0f, tab);   // all lanes
+            if (c0 + u < nch) {
+                L = __fmaf_rn(l[u], al, L);
+                O = __fmaf_rn(o[u], al, O);
+            }
+        }
+    }
+    return f2bf(__fdiv_rn(O, L));
+}
+
 // CL (cluster mode): the chunk CTAs of one (column, kv head) form a cluster; chunk 0 (the leader)
 // receives every other chunk's (m, l, o) by st.async into its K/V buffer once it has finished with
 // it, combines them in chunk order and writes the output: no workspace, no ticket, no grid-wide
@@ -362,17 +401,7 @@ __global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, flo
         const int ch = tid + j * kNT;
         if (ch >= CHAINS) continue;
         const int g = ch / HD, d = ch % HD;
-        const float* base = wsb + g * (HD + 4);
-        float M = -FLT_MAX;
-        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(base + cc * cstride));
-        float L = 0.0f, O = 0.0f;
-        for (int cc = 0; cc < nch; ++cc) {
-            const float* w = base + cc * cstride;
-            const float al = det_expf_shfl(__fsub_rn(__ldcg(w), M), tab);
-            L = __fmaf_rn(__ldcg(w + 1), al, L);
-            O = __fmaf_rn(__ldcg(w + 4 + d), al, O);
-        }
-        outp[ch] = f2bf(__fdiv_rn(O, L));
+        outp[ch] = combine_ws_chain(wsb + g * (HD + 4), cstride, nch, d, tab);
     }
 }
 
@@ -407,10 +436,230 @@ cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
     return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G, CL>, a, scale);
 }
 
+// Prefill: one CTA per (chunk, kv head, block of Q = 16/G consecutive query columns): the chunk's
+// K/V is loaded once for the block instead of once per query. Per (query, head) row the
+// arithmetic is chunk_scores / chunk_softmax / chunk_pv's: each thread evaluates four score trees
+// over one K row (the K vector unpacked once for the four), and the PV chains of a dimension share
+// each V element. Chunk partials go to the workspace; the CTA completing a query's chunk count
+// (ticket per column) combines it exactly as attn_chunk_kernel's ticket combine.
+template <int HD, int G>
+__global__ void __launch_bounds__(kNT) attn_prefill_kernel(const AttnParams a, float scale) {
+    constexpr int CH = kAttnChunk;
+    constexpr int Q = G >= 16 ? 1 : 16 / G;          // query columns per CTA
+    constexpr int R = Q * G;                         // (query, head) rows, 16
+    constexpr int NV = HD / 8;
+    constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
+    constexpr int SR = R * CH / kNT;                 // score rows per thread (4)
+    constexpr int PR = R * HD / kNT;                 // PV chains per thread
+    static_assert(kNT % CH == 0 && kNT % HD == 0 && R * CH % kNT == 0, "mapping");
+    extern __shared__ __align__(16) uint8_t pf_dsm[];
+    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(pf_dsm);
+    __nv_bfloat16* sV = sK + CH * HD;
+    float* sQ = reinterpret_cast<float*>(sV + CH * HD);   // [R][HD]
+    float* sS = sQ + R * HD;                               // [R][CH]
+    __shared__ float sM[R], sL[R];
+    __shared__ int s_pos[Q], s_slot[Q], s_n[Q], s_run[Q], s_last[Q];
+    pdl_wait();
+    pdl_trigger();
+    const int c = blockIdx.x, kvh = blockIdx.y, col0 = blockIdx.z * Q;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int p0 = c * CH;
+    if (tid < Q) {
+        const int col = col0 + tid;
+        const int pos = col < a.ncols ? a.col_pos[col] : -1;
+        s_pos[tid] = pos;
+        s_slot[tid] = pos >= 0 ? a.col_req[col] : -1;
+        s_n[tid] = pos >= p0 ? min(CH, pos + 1 - p0) : 0;
+    }
+    __syncthreads();
+    const ExpTab tab = exp_tab_lane();
+    for (int q0 = 0; q0 < Q;) {   // runs of queries of one request share the K/V chunk
+        int q1 = q0 + 1;
+        while (q1 < Q && s_slot[q1] == s_slot[q0]) ++q1;
+        int nmax = 0;
+        for (int q = q0; q < q1; ++q) nmax = max(nmax, s_n[q]);
+        if (s_slot[q0] < 0 || nmax == 0) {
+            q0 = q1;
+            continue;
+        }
+        if (tid < Q) s_run[tid] = tid >= q0 && tid < q1 ? s_n[tid] : 0;   // this run's rows only
+        const int* bt = a.block_table + static_cast<int64_t>(s_slot[q0]) * a.max_pages;
+        load_chunk_rows<HD>(a, bt, kvh, p0, 0, nmax, sK, sV, true, true, tid);
+        cp_async_commit();
+        for (int i = tid; i < (q1 - q0) * G * HD; i += kNT) {
+            const int q = q0 + i / (G * HD), rem = i % (G * HD);
+            sQ[q * G * HD + rem] = bf2f(a.q[static_cast<int64_t>(col0 + q) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD + rem]);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        {   // scores: position p, rows rg, rg + kNT/CH, ... (same tree as chunk_scores)
+            const int p = tid % CH, rg = tid / CH;
+            float stk[SR][DEPTH];
+            bool on[SR];
+#pragma unroll
+            for (int k = 0; k < SR; ++k) on[k] = p < s_run[(rg + k * (kNT / CH)) / G];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
+                const float kf[8] = {__uint_as_float(kv.x << 16), __uint_as_float(kv.x & 0xffff0000u),
+                                     __uint_as_float(kv.y << 16), __uint_as_float(kv.y & 0xffff0000u),
+                                     __uint_as_float(kv.z << 16), __uint_as_float(kv.z & 0xffff0000u),
+                                     __uint_as_float(kv.w << 16), __uint_as_float(kv.w & 0xffff0000u)};
+#pragma unroll
+                for (int k = 0; k < SR; ++k) {
+                    const int r = rg + k * (kNT / CH);
+                    const float4* q4 = reinterpret_cast<const float4*>(sQ + r * HD + v * 8);
+                    const float4 qa = q4[0], qb = q4[1];
+                    float pr[8] = {__fmul_rn(qa.x, kf[0]), __fmul_rn(qa.y, kf[1]), __fmul_rn(qa.z, kf[2]),
+                                   __fmul_rn(qa.w, kf[3]), __fmul_rn(qb.x, kf[4]), __fmul_rn(qb.y, kf[5]),
+                                   __fmul_rn(qb.z, kf[6]), __fmul_rn(qb.w, kf[7])};
+                    float carry = local_tree_sum<8>(pr);
+                    int lvl = 0;
+#pragma unroll
+                    for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[k][lvl], carry);
+                    stk[k][lvl] = carry;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < SR; ++k)
+                if (on[k]) sS[(rg + k * (kNT / CH)) * CH + p] = __fmul_rn(stk[k][DEPTH - 1], scale);
+        }
+        __syncthreads();
+        for (int r = warp; r < R; r += kNW) {   // chunk softmax per row (chunk_softmax's arithmetic)
+            const int n = s_run[r / G];
+            if (n == 0) continue;
+            constexpr int PPL = CH / 32;
+            float sv[PPL], e[PPL];
+            float m = -FLT_MAX;
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                const int p = lane * PPL + j;
+                sv[j] = p < n ? sS[r * CH + p] : 0.0f;
+                if (p < n) m = fmaxf(m, sv[j]);
+            }
+            m = warp_max(m);
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                const int p = lane * PPL + j;
+                const float ev = det_expf_shfl(p < n ? __fsub_rn(sv[j], m) : 0.0f, tab);
+                e[j] = p < n ? ev : kNegZero;
+                sS[r * CH + p] = e[j];
+            }
+            float l = local_tree_sum<PPL>(e);
+            l = warp_tree_sum(l);
+            if (lane == 0) {
+                sM[r] = m;
+                sL[r] = l;
+            }
+        }
+        __syncthreads();
+        {   // PV: dimension d, rows rb, rb + kNT/HD, ...: one V element feeds PR chains
+            const int d = tid % HD, rb = tid / HD;
+            const uint16_t* v16 = reinterpret_cast<const uint16_t*>(sV);
+            float acc[PR];
+            int nr[PR];
+            int nmin = CH;
+#pragma unroll
+            for (int k = 0; k < PR; ++k) {
+                acc[k] = 0.0f;
+                nr[k] = s_run[(rb + k * (kNT / HD)) / G];
+                nmin = min(nmin, nr[k]);
+            }
+            const float* srow = sS + rb * CH;   // row rb + k*(kNT/HD) at srow + k*(kNT/HD)*CH
+#pragma unroll 4
+            for (int p = 0; p < nmin; ++p) {   // every row active: no per-FMA guard
+                const float v = __uint_as_float(static_cast<uint32_t>(v16[p * HD + d]) << 16);
+#pragma unroll
+                for (int k = 0; k < PR; ++k) acc[k] = __fmaf_rn(srow[k * (kNT / HD) * CH + p], v, acc[k]);
+            }
+            for (int p = nmin; p < nmax; ++p) {   // the causal edge
+                const float v = __uint_as_float(static_cast<uint32_t>(v16[p * HD + d]) << 16);
+#pragma unroll
+                for (int k = 0; k < PR; ++k)
+                    if (p < nr[k]) acc[k] = __fmaf_rn(srow[k * (kNT / HD) * CH + p], v, acc[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < PR; ++k) {
+                const int r = rb + k * (kNT / HD), q = r / G, g = r % G;
+                if (nr[k] == 0) continue;
+                float* ws = a.ws + ((static_cast<int64_t>(col0 + q) * a.hkv + kvh) * a.max_chunks + c) * G * (HD + 4) +
+                            g * (HD + 4);
+                ws[4 + d] = acc[k];
+                if (d == 0) {
+                    ws[0] = sM[r];
+                    ws[1] = sL[r];
+                }
+            }
+        }
+        __syncthreads();
+        q0 = q1;
+    }
+    // per-column tickets: the CTA holding a column's last chunk partial combines that column
+    __threadfence();
+    __syncthreads();
+    if (tid < Q) {
+        s_last[tid] = 0;
+        if (s_n[tid] > 0) {
+            const int nch = (s_pos[tid] + CH) / CH;
+            int* t = a.tickets + static_cast<int64_t>(col0 + tid) * a.hkv + kvh;
+            if (atomicAdd(t, 1) == nch - 1) {
+                s_last[tid] = 1;
+                *t = 0;   // re-armed for the next launch
+            }
+        }
+    }
+    __syncthreads();
+    __threadfence();
+    for (int q = 0; q < Q; ++q) {
+        if (!s_last[q]) continue;   // block-uniform
+        const int nch = (s_pos[q] + CH) / CH;
+        const float* wsb = a.ws + (static_cast<int64_t>(col0 + q) * a.hkv + kvh) * a.max_chunks * G * (HD + 4);
+        const int64_t cstride = static_cast<int64_t>(G) * (HD + 4);
+        __nv_bfloat16* outp = a.out + static_cast<int64_t>(col0 + q) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
+        for (int ch = tid; ch < G * HD; ch += kNT) {   // whole warps: det_expf_shfl
+            const int g = ch / HD, d = ch % HD;
+            const float* base = wsb + g * (HD + 4);
+            if (nch == 1) {   // the combine weight is exp(0) == 1 exactly (as attn_chunk_kernel)
+                outp[ch] = f2bf(__fdiv_rn(__fmaf_rn(__ldcg(base + 4 + d), 1.0f, 0.0f), __fmaf_rn(__ldcg(base + 1), 1.0f, 0.0f)));
+                continue;
+            }
+            outp[ch] = combine_ws_chain(base, cstride, nch, d, tab);
+        }
+    }
+}
+
+template <int HD, int G>
+cudaError_t launch_prefill(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    constexpr int Q = G >= 16 ? 1 : 16 / G;
+    constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2 + static_cast<size_t>(Q * G) * HD * 4 +
+                           static_cast<size_t>(Q * G) * kAttnChunk * 4;
+    static std::atomic<uint64_t> attr_devs{0};
+    int dev = 0;
+    if (attrs_needed(attr_devs, &dev)) {
+        cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(dsm));
+        if (e != cudaSuccess) return e;
+        attrs_done(attr_devs, dev);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.max_chunks, a.hkv, (a.ncols + Q - 1) / Q);
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = dsm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(HD)));
+    return cudaLaunchKernelEx(&cfg, attn_prefill_kernel<HD, G>, a, scale);
+}
+
 // Cluster combine when the chunks of a (column, kv head) fit one cluster and the pushed partials
 // fit the leader's K/V buffer; the workspace/ticket combine otherwise.
 template <int HD, int G>
 cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    if (!a.decode && a.prefill_blocks) return launch_prefill<HD, G>(a, stream, pdl);
     const bool cl = a.max_chunks <= kMaxClusterChunks &&
                     static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 <= 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
     return cl ? launch_hgc<HD, G, true>(a, stream, pdl) : launch_hgc<HD, G, false>(a, stream, pdl);

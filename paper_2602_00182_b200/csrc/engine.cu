@@ -113,6 +113,7 @@ struct Engine {
     unsigned l2pf_mask = 2;
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
     int max_nsub = 0;     // GemmParams::max_nsub
+    bool prefill_blocks = true;   // AttnParams::prefill_blocks
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
     int64_t l2pf_cap = 16ll << 20;
 
@@ -377,6 +378,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_pages = E->pages_per_slot;
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
+        a.prefill_blocks = E->prefill_blocks ? 1 : 0;
         a.trace = E->trace_buf;
         a.trace_tag = kProfAttn;
         if (pf & 1u) {
@@ -1216,6 +1218,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
+    else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);

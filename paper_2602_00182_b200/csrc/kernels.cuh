@@ -50,6 +50,7 @@ struct AttnParams {
     int* tickets;                  // [ncols][hkv], zero-initialised; reset by the combining CTA
     int ncols, hq, hkv, hd, page, max_pages, max_chunks;
     int decode;                    // 1: every column's positions < pos were written by earlier launches
+    int prefill_blocks;            // prefill: query blocks share each K/V chunk (attn_prefill_kernel)
     const void* l2pf;              // optional: bytes warmed into L2 at kernel start (the o weights)
     int64_t l2pf_bytes;
     TraceRec* trace;        // optional per-CTA timeline (timing instrumentation)
