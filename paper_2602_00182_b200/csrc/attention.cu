@@ -443,7 +443,7 @@ cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
 // each V element. Chunk partials go to the workspace; the CTA completing a query's chunk count
 // (ticket per column) combines it exactly as attn_chunk_kernel's ticket combine.
 template <int HD, int G>
-__global__ void __launch_bounds__(kNT, 3) attn_prefill_kernel(const AttnParams a, float scale) {
+__global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a, float scale) {
     constexpr int CH = kAttnChunk;
     constexpr int Q = G >= 16 ? 1 : 16 / G;          // query columns per CTA
     constexpr int R = Q * G;                         // (query, head) rows, 16
