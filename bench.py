@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--prompt", type=int, default=512)
     ap.add_argument("--gen", type=int, default=256)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
     ap.add_argument("--cpu-sample-prompt", type=int, default=4)
     ap.add_argument("--cpu-sample-gen", type=int, default=2)
@@ -220,18 +220,20 @@ def run_ours(args, rank: int, world: int, local: int):
     decode_tok_s = (toks - args.batch * args.steps) / (decode_ms / 1000.0) if decode_ms > 0 else None
 
     # ---- end to end through the C-ABI with host buffers: prompt H2D, logits+tokens D2H, SHA-256
-    hashes, e2e_s, h2d, d2h, hash_ms = [], 0.0, 0, 0, 0.0
+    # e2e_steps batches of the same requests in ONE call with continuous batching (batch slots =
+    # args.batch): a finished request's logits D2H and SHA-256 run on a worker thread while the next
+    # request decodes, as a server would run them; the bytes of every request are unchanged.
     replicas.barrier(local)
-    for _ in range(args.e2e_steps):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, _, hs = eng.generate(prompts, pols, seeds, want_logits=False, want_hash=True)
-        e2e_s += time.perf_counter() - t0
-        hashes.append(hs)
-        st = eng.last_stats
-        h2d += st.h2d_bytes + sum(p.nbytes for p in prompts)
-        d2h += st.d2h_bytes
-        hash_ms += st.hash_ms
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, _, hs_all = eng.generate(prompts * args.e2e_steps, pols * args.e2e_steps, seeds * args.e2e_steps,
+                                batch_size=args.batch, want_logits=False, want_hash=True, continuous=True)
+    e2e_s = time.perf_counter() - t0
+    st = eng.last_stats
+    h2d = st.h2d_bytes + sum(p.nbytes for p in prompts) * args.e2e_steps
+    d2h = st.d2h_bytes
+    hash_ms = st.hash_ms
+    hashes = [hs_all[i * args.batch:(i + 1) * args.batch] for i in range(args.e2e_steps)]
     e2e_max = replicas.max_over_ranks(e2e_s, local)
     e2e_value = replicas.sum_over_ranks(args.gen * args.batch * args.e2e_steps, local) / e2e_max
     replay_rate = float(np.mean([h == hashes[0] for h in hashes]))
@@ -294,7 +296,8 @@ def run_ours(args, rank: int, world: int, local: int):
                    "l2": "inputs larger than L2: 16 GB of weights streamed every decode step (L2 126 MB)"},
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": h2d // max(args.e2e_steps, 1),
                 "d2h_bytes_per_step": d2h // max(args.e2e_steps, 1),
-                "what": "detgpu_generate with host prompt buffers; tokens + f32 logits D2H; SHA-256 receipt",
+                "what": "detgpu_generate (continuous batching, e2e_steps copies of the batch in one call) with host "
+                        "prompt buffers; tokens + f32 logits D2H; SHA-256 receipt (worker threads)",
                 "hash_ms_per_step": hash_ms / max(args.e2e_steps, 1)},
         "e2e_receipt_v2": {"value": e2e_v2, "unit": "tok/s", "d2h_bytes_per_step": v2_d2h // max(args.e2e_steps, 1),
                            "hash_ms_per_step": v2_hash_ms / max(args.e2e_steps, 1),

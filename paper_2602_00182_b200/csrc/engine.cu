@@ -96,6 +96,14 @@ struct Engine {
     // pinned staging for D2H
     float* pinned[2] = {nullptr, nullptr};
     size_t pinned_floats = 0;
+    // pinned host buffers for traces hashed off the decode loop (collect_slot), reused once their
+    // hashing task is done
+    struct HashBuf {
+        float* p = nullptr;
+        size_t cap = 0;
+        std::shared_future<void> busy;
+    };
+    std::vector<HashBuf> hash_bufs;
     // decode graphs keyed by (ncols, slot_stride)
     std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
     uint64_t launches_per_step = 0;
@@ -129,6 +137,10 @@ struct Engine {
         for (void* p : allocs) cudaFree(p);
         if (trace) cudaFree(trace);
         if (trace_buf) cudaFree(trace_buf);
+        for (auto& hb : hash_bufs) {
+            if (hb.busy.valid()) hb.busy.wait();
+            if (hb.p) cudaFreeHost(hb.p);
+        }
         if (tok_hist) cudaFree(tok_hist);
         if (d_roots) cudaFree(d_roots);
         if (d_steps) cudaFree(d_steps);
@@ -731,21 +743,46 @@ int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* l
     if (want_hash && hashers != nullptr && T > 0) {
         // continuous batching: copy the slot's trace out and hash it on a worker thread, so that
         // the v1 SHA-256 (sequential, ~71 ms per 8B request) does not stall the decode loop
-        std::shared_ptr<std::vector<float>> own;
-        float* dst = logits_out;
-        if (dst == nullptr) {
-            own = std::make_shared<std::vector<float>>(size_t(T) * V);
-            dst = own->data();
-        }
+        const size_t n = size_t(T) * V;
         Timer tw;
-        ENG_CUDA(cudaMemcpy(dst, E->trace + size_t(slot) * E->slot_stride, sizeof(float) * size_t(T) * V,
-                            cudaMemcpyDeviceToHost));
+        float* dst = logits_out;
+        Engine::HashBuf* hb = nullptr;
+        if (dst == nullptr) {   // a pinned buffer whose previous hash is done (at most three)
+            for (auto& b : E->hash_bufs)
+                if (!b.busy.valid() || b.busy.wait_for(std::chrono::seconds(0)) == std::future_status::ready) {
+                    hb = &b;
+                    break;
+                }
+            if (hb == nullptr && E->hash_bufs.size() < 3) {
+                E->hash_bufs.emplace_back();
+                hb = &E->hash_bufs.back();
+            }
+            if (hb == nullptr) {
+                hb = &E->hash_bufs.front();
+                hb->busy.wait();
+            }
+            if (hb->cap < n) {
+                if (hb->p) cudaFreeHost(hb->p);
+                hb->p = nullptr;
+                hb->cap = 0;
+                ENG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb->p), sizeof(float) * n, cudaHostAllocDefault));
+                hb->cap = n;
+            }
+            dst = hb->p;
+        }
+        ENG_CUDA(cudaMemcpy(dst, E->trace + size_t(slot) * E->slot_stride, sizeof(float) * n, cudaMemcpyDeviceToHost));
         copy_ms += tw.ms();
-        if (st) st->d2h_bytes += 4 * size_t(T) * V;
+        if (st) st->d2h_bytes += 4 * n;
         auto tk = std::make_shared<std::vector<uint32_t>>(toks.begin(), toks.begin() + T);
-        hashers->push_back(std::async(std::launch::async, [tk, own, dst, T, V, out_hash]() {
+        std::future<void> f = std::async(std::launch::async, [tk, dst, T, V, out_hash]() {
             hash_canonical(tk->data(), T, dst, static_cast<uint32_t>(V), out_hash);
-        }));
+        });
+        if (hb != nullptr) {
+            hb->busy = f.share();
+            hashers->push_back(std::async(std::launch::deferred, [sf = hb->busy]() { sf.wait(); }));
+        } else {
+            hashers->push_back(std::move(f));
+        }
         if (st) st->d2h_ms += static_cast<float>(copy_ms);
         return DETGPU_OK;
     }
