@@ -133,6 +133,10 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *                 1 o->gate/up, 2 gate/up->down, 3 down->next QKV, 4 QKV->o)
  *   "l2pf_cap_mb" cap on the bytes one kernel warms
  *   "pdl"         programmatic dependent launch on (1) / off (0)
+ *   "prefill_blocks" prefill attention on query blocks sharing each K/V chunk (1, default) or
+ *                 one query per CTA (0)
+ *   "attn_cluster_max_cols" decode attention combines chunks in a cluster up to this many
+ *                 columns (default 8), in the workspace/ticket path above (0: always cluster)
  *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor

@@ -660,7 +660,8 @@ cudaError_t launch_prefill(const AttnParams& a, cudaStream_t stream, bool pdl) {
 template <int HD, int G>
 cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
     if (!a.decode && a.prefill_blocks) return launch_prefill<HD, G>(a, stream, pdl);
-    const bool cl = a.max_chunks <= kMaxClusterChunks &&
+    // many columns: the workspace/ticket combine schedules better than 12-CTA clusters
+    const bool cl = (a.cluster_max_cols <= 0 || a.ncols <= a.cluster_max_cols) && a.max_chunks <= kMaxClusterChunks &&
                     static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 <= 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
     return cl ? launch_hgc<HD, G, true>(a, stream, pdl) : launch_hgc<HD, G, false>(a, stream, pdl);
 }

@@ -122,6 +122,7 @@ struct Engine {
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
+    int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
     int64_t l2pf_cap = 16ll << 20;
 
@@ -391,6 +392,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.max_chunks = E->max_chunks;
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
         a.prefill_blocks = E->prefill_blocks ? 1 : 0;
+        a.cluster_max_cols = E->attn_cluster_max_cols;
         a.trace = E->trace_buf;
         a.trace_tag = kProfAttn;
         if (pf & 1u) {
@@ -1256,6 +1258,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
+    else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);
