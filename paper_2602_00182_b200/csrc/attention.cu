@@ -200,7 +200,7 @@ __device__ __forceinline__ __nv_bfloat16 combine_ws_chain(const float* base, int
 // it, combines them in chunk order and writes the output: no workspace, no ticket, no grid-wide
 // round trip. Same arithmetic as the ticket combine below.
 template <int HD, int G, bool CL>
-__global__ void __launch_bounds__(kNT) attn_chunk_kernel(const AttnParams a, float scale) {
+__global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, float scale) {   // <= 40 registers: six CTAs per SM
     constexpr int CH = kAttnChunk;
     constexpr int E = HD / 32;                       // q/k elements per lane in a dot product
     constexpr int CHAINS = G * HD;                   // (head, d) accumulators of the PV product
