@@ -675,6 +675,8 @@ size_t attn_workspace_bytes(const AttnParams& a) {
 
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl) {
     if (a.hkv <= 0 || a.hq % a.hkv != 0 || a.page < 16 || a.page % 16 != 0) return cudaErrorInvalidValue;
+    if (a.stream_min_cols > 0 && a.ncols >= a.stream_min_cols && attention_stream_supported(a))
+        return launch_attention_stream(a, stream, pdl);
     const int G = a.hq / a.hkv;
     if (a.hd == 128) {
         switch (G) {

@@ -59,6 +59,7 @@ struct Engine {
     // weights
     __nv_bfloat16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
     CUtensorMap tm_lm;
+    CUtensorMap tm_kpool, tm_vpool;   // whole K / V pools as [rows][hd] (streamed decode attention)
     std::vector<Layer> layers;
     uint64_t n_params = 0;
     // activations
@@ -122,6 +123,7 @@ struct Engine {
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
+    int attn_stream_min_cols = 9;    // AttnParams::stream_min_cols (0: off)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
     int64_t l2pf_cap = 16ll << 20;
@@ -234,6 +236,9 @@ int init_buffers(Engine* E) {
     const size_t per_layer = size_t(E->total_pages) * kPage * kd;
     ENG_CUDA(E->alloc(&E->kpool, per_layer * c.L));
     ENG_CUDA(E->alloc(&E->vpool, per_layer * c.L));
+    if (!make_tmap_bf16(&E->tm_kpool, E->kpool, c.hd, per_layer * c.L / c.hd, 64) ||
+        !make_tmap_bf16(&E->tm_vpool, E->vpool, c.hd, per_layer * c.L / c.hd, 64))
+        return fail(E, DETGPU_ECUDA, "tensor map (kv pool)");
     std::vector<int> bt(size_t(B) * E->pages_per_slot);
     for (size_t i = 0; i < bt.size(); ++i) bt[i] = static_cast<int>(i);
     ENG_CUDA(E->alloc(&E->block_table, bt.size()));
@@ -393,6 +398,10 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
         a.prefill_blocks = E->prefill_blocks ? 1 : 0;
         a.cluster_max_cols = E->attn_cluster_max_cols;
+        a.tm_k = &E->tm_kpool;
+        a.tm_v = &E->tm_vpool;
+        a.kv_row0 = static_cast<int64_t>(per_layer / c.hd) * l;
+        a.stream_min_cols = E->attn_stream_min_cols;
         a.trace = E->trace_buf;
         a.trace_tag = kProfAttn;
         if (pf & 1u) {
@@ -1259,6 +1268,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
+    else if (std::strcmp(name, "attn_stream_min_cols") == 0) E->attn_stream_min_cols = static_cast<int>(value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);

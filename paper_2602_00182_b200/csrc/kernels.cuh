@@ -2,6 +2,7 @@
 #pragma once
 #include "trace.h"
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -56,9 +57,18 @@ struct AttnParams {
     int64_t l2pf_bytes;
     TraceRec* trace;        // optional per-CTA timeline (timing instrumentation)
     uint32_t trace_tag;
+    // streamed decode attention (attention_stream.cu): 2D tensor maps over the whole K / V pools
+    // ([rows][hd], 64x64 boxes, 128B swizzle), this layer's first row, and the column count from
+    // which it replaces attn_chunk_kernel (0: never)
+    const CUtensorMap* tm_k;
+    const CUtensorMap* tm_v;
+    int64_t kv_row0;
+    int stream_min_cols;
 };
 size_t attn_workspace_bytes(const AttnParams& a);
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);
+bool attention_stream_supported(const AttnParams& a);
+cudaError_t launch_attention_stream(const AttnParams& a, cudaStream_t stream, bool pdl);
 
 // ---- softmax + decode ----
 struct DevPolicy {

@@ -211,3 +211,30 @@ def test_tiny_context_beyond_cluster_path(tiny_oracle):
     assert (logits[0].view(np.uint32) == ol.view(np.uint32)).all()
     assert h[0] == O.out_hash(ot, ol)
     eng.close()
+
+
+def test_streamed_decode_attention_bit_exact(tiny_oracle):
+    """The streamed decode attention (persistent CTAs, TMA ring, attention_stream.cu) against the
+    per-chunk kernels and the oracle: ragged contexts from 1 to 900 positions (1..15 chunks, a
+    column split across CTAs), every decode step through the streamed kernel."""
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    eng = Engine("llama-tiny:model-a", "b200", max_batch=24, max_context=1024)
+    lens = [1, 2, 63, 64, 65, 127, 128, 129, 300, 511, 512, 513, 700, 899, 17, 5, 250, 640, 33, 96]
+    prompts = [_prompt(500 + i, n, eng.vocab) for i, n in enumerate(lens)]
+    pols = [[DecodePolicy.greedy(5), DecodePolicy.nucleus(0.9, 5)][i % 2] for i in range(len(lens))]
+    seeds = [7 + i for i in range(len(lens))]
+    eng.set_option("attn_stream_min_cols", 0)
+    ref_t, ref_l, ref_h = eng.generate(prompts, pols, seeds, batch_size=len(lens))
+    for min_cols in (1, 9):
+        eng.set_option("attn_stream_min_cols", min_cols)
+        t, l, h = eng.generate(prompts, pols, seeds, batch_size=len(lens))
+        assert h == ref_h, f"attn_stream_min_cols {min_cols}"
+        for i in range(len(lens)):
+            assert np.array_equal(l[i].view(np.uint32), ref_l[i].view(np.uint32)), (min_cols, i)
+    for i in (0, 4, 13):
+        ot, ol = tiny_oracle.generate(prompts[i], kind=0 if i % 2 == 0 else 2, p=None if i % 2 == 0 else 0.9,
+                                      max_tokens=5, seed=seeds[i])
+        assert t[i].tolist() == ot.tolist(), i
+        assert (l[i].view(np.uint32) == ol.view(np.uint32)).all(), i
+    eng.close()
