@@ -67,7 +67,6 @@ __device__ __forceinline__ void chunk_scores(const __nv_bfloat16* sK, const floa
     constexpr int CH = kAttnChunk;
     constexpr int NV = HD / 8;                       // 16-byte vectors per row
     constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
-    const float4* q4 = reinterpret_cast<const float4*>(sQ);
     for (int idx = tid; idx < G * CH; idx += kNT) {
         const int p = idx % CH, g = idx / CH;
         if (p >= n) continue;
@@ -75,12 +74,8 @@ __device__ __forceinline__ void chunk_scores(const __nv_bfloat16* sK, const floa
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
-            const float4 qa = q4[(g * HD + v * 8) / 4], qb = q4[(g * HD + v * 8) / 4 + 1];
-            float pr[8] = {__fmul_rn(qa.x, __uint_as_float(kv.x << 16)), __fmul_rn(qa.y, __uint_as_float(kv.x & 0xffff0000u)),
-                           __fmul_rn(qa.z, __uint_as_float(kv.y << 16)), __fmul_rn(qa.w, __uint_as_float(kv.y & 0xffff0000u)),
-                           __fmul_rn(qb.x, __uint_as_float(kv.z << 16)), __fmul_rn(qb.y, __uint_as_float(kv.z & 0xffff0000u)),
-                           __fmul_rn(qb.z, __uint_as_float(kv.w << 16)), __fmul_rn(qb.w, __uint_as_float(kv.w & 0xffff0000u))};
-            float carry = local_tree_sum<8>(pr);
+            float carry = qk_block8(kv, *reinterpret_cast<const ulonglong2*>(sQ + g * HD + v * 8),
+                                    *reinterpret_cast<const ulonglong2*>(sQ + g * HD + v * 8 + 4));
             int lvl = 0;
 #pragma unroll
             for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[lvl], carry);
@@ -208,7 +203,7 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     extern __shared__ __align__(16) uint8_t attn_dsm[];
     __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_dsm);
     __nv_bfloat16* sV = sK + CH * HD;
-    __shared__ float sQ[G * HD];
+    __shared__ __align__(16) float sQ[G * HD];
     __shared__ float sS[G * CH];
     __shared__ float sM[G], sL[G];
     __shared__ int s_last;
@@ -228,6 +223,7 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
                              m);
         }
     } tr{a, {a.trace != nullptr ? globaltimer_ns() : 0}};
+    const ExpTab tab = exp_tab_lane();   // issued before the dependency wait: off the critical path
     if (threadIdx.x == 0)
         l2_prefetch_slice(a.l2pf, a.l2pf_bytes, c + gridDim.x * (kvh + gridDim.y * col),
                           gridDim.x * gridDim.y * gridDim.z);
@@ -284,7 +280,7 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     }
     cp_async_commit();
     const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    for (int i = tid; i < G * HD; i += kNT) sQ[i] = bf2f(qsrc[i]);
+    for (int i = tid; i < G * HD; i += kNT) sQ[qperm(i)] = bf2f(qsrc[i]);   // quads in qk_block8 order
     cp_async_wait_all();
     __syncthreads();
     tr.mark(2);   // K/V chunk and q in shared memory
@@ -293,7 +289,6 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     __syncthreads();
     tr.mark(3);   // scores
 
-    const ExpTab tab = exp_tab_lane();
     chunk_softmax<G>(sS, sM, sL, n, warp, lane, tab);
     __syncthreads();
     tr.mark(4);   // softmax
@@ -322,12 +317,11 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
                     mbar_wait(&s_bar[0], 0);
                 }
                 __syncthreads();
-                const ExpTab tab2 = exp_tab_lane();
                 if (tid < ((G * kMaxClusterChunks + 31) & ~31)) {   // warp-uniform: det_expf_shfl needs all lanes
                     const int g = tid / kMaxClusterChunks, cc = tid % kMaxClusterChunks;
                     const bool ok = g < G && cc < nch;
                     const float m = !ok ? 0.0f : cc == 0 ? sM[g] : recv[(cc - 1) * BLK + g];
-                    const float al = det_expf_shfl(ok ? __fsub_rn(m, s_mx[g < G ? g : 0]) : 0.0f, tab2);
+                    const float al = det_expf_shfl(ok ? __fsub_rn(m, s_mx[g < G ? g : 0]) : 0.0f, tab);
                     if (ok) s_al[g][cc] = al;
                 }
                 __syncthreads();

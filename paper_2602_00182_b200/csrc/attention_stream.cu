@@ -69,23 +69,6 @@ __device__ __forceinline__ uint32_t swz(int p, int d) {
     return static_cast<uint32_t>(half * (kCH * 128) + p * 128 + ((((dd >> 3) ^ (p & 7))) << 4) + (dd & 7) * 2);
 }
 
-// packed f32x2 arithmetic (FMUL2 / FFMA2): each lane of the pair is an IEEE round-to-nearest f32
-// operation, bit-identical to the scalar __fmul_rn / __fmaf_rn
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-// fma(a, b, c) per lane. Used only where a*b is exact in f32 (a product of two bf16 values has at
-// most 16 significant bits), so it equals add(round(a*b), c) bit for bit.
-__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ float lo32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
-__device__ __forceinline__ float hi32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
-
 struct ChunkInfo {
     int col, kvh, c, n, nch;
     int key;     // the item's first chunk in this CTA's range, relative to the range start
@@ -277,19 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const uint4 kv = *reinterpret_cast<const uint4*>(st + kbase + (((v & 7) ^ (p & 7)) << 4) + (v >> 3) * (kCH * 128));
-                // pairs {k0,k2}, {k1,k3}, {k4,k6}, {k5,k7} (the q quads are stored 0,2,1,3)
-                const uint64_t k02 = (static_cast<uint64_t>(kv.y << 16) << 32) | (kv.x << 16);
-                const uint64_t k13 = (static_cast<uint64_t>(kv.y & 0xffff0000u) << 32) | (kv.x & 0xffff0000u);
-                const uint64_t k46 = (static_cast<uint64_t>(kv.w << 16) << 32) | (kv.z << 16);
-                const uint64_t k57 = (static_cast<uint64_t>(kv.w & 0xffff0000u) << 32) | (kv.z & 0xffff0000u);
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8);       // {q0,q2},{q1,q3}
-                    const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8 + 4);   // {q4,q6},{q5,q7}
-                    // {p0+p1, p2+p3}, {p4+p5, p6+p7}: exact products, so fma == add of the products
-                    const uint64_t s0 = fma2(qa.x, k02, mul2(qa.y, k13));
-                    const uint64_t s1 = fma2(qb.x, k46, mul2(qb.y, k57));
-                    float carry = __fadd_rn(__fadd_rn(lo32(s0), hi32(s0)), __fadd_rn(lo32(s1), hi32(s1)));
+                    float carry = qk_block8(kv, *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8),
+                                            *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8 + 4));
                     int lvl = 0;
 #pragma unroll
                     for (int bb = v; bb & 1; bb >>= 1, ++lvl) carry = __fadd_rn(stk[g][lvl], carry);

@@ -62,8 +62,20 @@ __device__ __forceinline__ float det_expf(float x) {
 struct ExpTab {
     uint32_t lo, hi;
 };
+// The same 32 entries in global memory: a warp fetches them with one coalesced 256-byte load (a
+// __constant__ read with 32 different addresses is serialised); call it early, off the critical path.
+__device__ const unsigned long long kExp2TabG[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
+};
 __device__ __forceinline__ ExpTab exp_tab_lane() {
-    const unsigned long long t = kExp2Tab[threadIdx.x & 31];
+    const unsigned long long t = __ldg(&kExp2TabG[threadIdx.x & 31]);
     return ExpTab{static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32)};
 }
 __device__ __forceinline__ float det_expf_shfl(float x, ExpTab tab) {
@@ -99,6 +111,39 @@ __device__ __forceinline__ float det_expf_shfl(float x, ExpTab tab) {
     }
     return res;
 }
+
+// packed f32x2 arithmetic (FMUL2 / FFMA2): each lane of the pair is an IEEE round-to-nearest f32
+// operation, bit-identical to the scalar __fmul_rn / __fmaf_rn
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// fma(a, b, c) per lane. Used only where a*b is exact in f32 (a product of two bf16 values has at
+// most 16 significant bits), so it equals add(round(a*b), c) bit for bit.
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float lo32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+
+// Canonical 8-product block of a q.k dot product (local_tree_sum<8> of the exact products):
+// ((p0+p1)+(p2+p3)) + ((p4+p5)+(p6+p7)), p_i = q_i * k_i with k_i the 8 bf16 values of `kv` and q
+// stored as f32 quads in the order q0 q2 q1 q3 | q4 q6 q5 q7 (qa, qb). Products of two bf16
+// values are exact in f32, so the packed fma equals the sum of the rounded products.
+__device__ __forceinline__ float qk_block8(uint4 kv, ulonglong2 qa, ulonglong2 qb) {
+    const uint64_t k02 = (static_cast<uint64_t>(kv.y << 16) << 32) | (kv.x << 16);
+    const uint64_t k13 = (static_cast<uint64_t>(kv.y & 0xffff0000u) << 32) | (kv.x & 0xffff0000u);
+    const uint64_t k46 = (static_cast<uint64_t>(kv.w << 16) << 32) | (kv.z << 16);
+    const uint64_t k57 = (static_cast<uint64_t>(kv.w & 0xffff0000u) << 32) | (kv.z & 0xffff0000u);
+    const uint64_t s0 = fma2(qa.x, k02, mul2(qa.y, k13));   // {p0+p1, p2+p3}
+    const uint64_t s1 = fma2(qb.x, k46, mul2(qb.y, k57));   // {p4+p5, p6+p7}
+    return __fadd_rn(__fadd_rn(lo32(s0), hi32(s0)), __fadd_rn(lo32(s1), hi32(s1)));
+}
+// index of q element i in the permuted quad layout qk_block8 reads (swap 1 <-> 2 in each quad)
+__host__ __device__ constexpr int qperm(int i) { return (i & ~3) | ((i & 3) == 1 ? 2 : (i & 3) == 2 ? 1 : (i & 3)); }
 
 // ------------------------------------------------------------------ bf16
 __device__ __forceinline__ __nv_bfloat16 f2bf(float v) { return __float2bfloat16_rn(v); }

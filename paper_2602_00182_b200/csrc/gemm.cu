@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     using C = Cfg<NSUB>;
     constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned (128B-swizzled tiles); offset arithmetic on the shared array keeps every
+    // access to it an LDS/STS (a pointer rebuilt from an integer would be generic)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NSUB * B_BYTES + C::BC_EXTRA);

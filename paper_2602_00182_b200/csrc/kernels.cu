@@ -251,200 +251,6 @@ __global__ void init_kernel(__nv_bfloat16* dst, uint64_t seed, int64_t rows, int
     }
 }
 
-#if 0  // superseded by attention.cu
-// ------------------------------------------------------------------ attention
-// One CTA per (chunk, kv head, query column); G = hq/hkv query heads share the K/V chunk.
-//   s_p = tree_d(q_d * k_pd) * scale                 (products exact: bf16 x bf16)
-//   m = max_p s_p ; e_p = exp(s_p - m) ; l = tree_p(e_p) ; o_d = fma-chain_p(e_p * v_pd)
-// Partials (m, l, o) combined across chunks in chunk order by attn_combine_kernel.
-template <int HD>
-__global__ void __launch_bounds__(128) attn_chunk_kernel(const AttnParams a, float scale) {
-    constexpr int CH = kAttnChunk;
-    constexpr int E = HD / 32;
-    extern __shared__ __align__(16) uint8_t attn_dsm[];
-    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_dsm);
-    __nv_bfloat16* sV = sK + CH * HD;
-    __shared__ float sQ[8 * HD];
-    __shared__ float sS[8 * CH];
-    __shared__ float sM[8], sL[8];
-    pdl_trigger();
-    const int c = blockIdx.x, kvh = blockIdx.y, col = blockIdx.z;
-    pdl_wait();
-    const int pos = a.col_pos[col];
-    if (pos < 0) return;
-    const int ctx = pos + 1;
-    const int p0 = c * CH;
-    if (p0 >= ctx) return;
-    const int n = min(CH, ctx - p0);
-    const int G = a.hq / a.hkv;
-    const int slot = a.col_req[col];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-    const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    // K/V rows of this chunk: look up the (at most CH/page) page ids once, then stream all 16-byte
-    // vectors with cp.async (no dependent global round trip per row).
-    constexpr int VPR = HD * 2 / 16;   // 16-byte vectors per row
-    {
-        int pid[CH / 16];
-        const int npg = (n + a.page - 1) / a.page;
-        for (int j = 0; j < npg; ++j) pid[j] = a.block_table[static_cast<int64_t>(slot) * a.max_pages + (p0 / a.page) + j];
-        for (int i = tid; i < n * VPR; i += 128) {
-            const int r = i / VPR, v = i % VPR;
-            const int p = p0 + r;
-            const int64_t off = ((static_cast<int64_t>(pid[r / a.page]) * a.hkv + kvh) * a.page + p % a.page) * HD;
-            cp_async_16(sK + r * HD + v * 8, a.kcache + off + v * 8);
-            cp_async_16(sV + r * HD + v * 8, a.vcache + off + v * 8);
-        }
-        cp_async_commit();
-    }
-    for (int i = tid; i < G * HD; i += 128) sQ[i] = bf2f(qsrc[i]);
-    cp_async_wait_all();
-    __syncthreads();
-
-    // scores: two positions per warp per iteration, all G heads, 2G interleaved butterflies
-    for (int p = warp * 2; p < n; p += 8) {
-        const bool two = p + 1 < n;
-        float kv0[E], kv1[E];
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            kv0[j] = bf2f(sK[p * HD + lane * E + j]);
-            kv1[j] = two ? bf2f(sK[(p + 1) * HD + lane * E + j]) : 0.0f;
-        }
-        float s0[8], s1[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            if (g < G) {
-                float pr0[E], pr1[E];
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    const float qv = sQ[g * HD + lane * E + j];
-                    pr0[j] = __fmul_rn(qv, kv0[j]);
-                    pr1[j] = __fmul_rn(qv, kv1[j]);
-                }
-                s0[g] = local_tree_sum<E>(pr0);
-                s1[g] = local_tree_sum<E>(pr1);
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < G) {
-                    s0[g] = __fadd_rn(s0[g], __shfl_xor_sync(0xffffffffu, s0[g], off));
-                    s1[g] = __fadd_rn(s1[g], __shfl_xor_sync(0xffffffffu, s1[g], off));
-                }
-            }
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < G) {
-                    sS[g * CH + p] = __fmul_rn(s0[g], scale);
-                    if (two) sS[g * CH + p + 1] = __fmul_rn(s1[g], scale);
-                }
-            }
-        }
-    }
-    __syncthreads();
-
-    for (int g = warp; g < G; g += 4) {
-        float sv[4];
-        float m = -FLT_MAX;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int p = lane * 4 + j;
-            sv[j] = p < n ? sS[g * CH + p] : 0.0f;
-            if (p < n) m = fmaxf(m, sv[j]);
-        }
-        m = warp_max(m);
-        float e[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int p = lane * 4 + j;
-            e[j] = p < n ? det_expf(__fsub_rn(sv[j], m)) : kNegZero;
-            sS[g * CH + p] = e[j];
-        }
-        float l = local_tree_sum<4>(e);
-        l = warp_tree_sum(l);
-        if (lane == 0) {
-            sM[g] = m;
-            sL[g] = l;
-        }
-    }
-    __syncthreads();
-
-    // o_d = fma chain over the chunk's positions in order; thread owns (d, heads g = t/HD + k*128/HD)
-    constexpr int GPT = (8 * HD + 127) / 128;   // max heads per thread
-    const int d = tid % HD, g0 = tid / HD, gstep = 128 / HD;
-    float acc[GPT];
-#pragma unroll
-    for (int k = 0; k < GPT; ++k) acc[k] = 0.0f;
-#pragma unroll 4
-    for (int p = 0; p < n; ++p) {
-        const float v = bf2f(sV[p * HD + d]);
-#pragma unroll
-        for (int k = 0; k < GPT; ++k) {
-            const int g = g0 + k * gstep;
-            if (g < G) acc[k] = __fmaf_rn(sS[g * CH + p], v, acc[k]);
-        }
-    }
-    const int nch = (ctx + CH - 1) / CH;
-    __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    if (nch == 1) {
-        // single chunk: combine weight exp(0) == 1 exactly, so out = o / l directly
-#pragma unroll
-        for (int k = 0; k < GPT; ++k) {
-            const int g = g0 + k * gstep;
-            if (g < G) outp[g * HD + d] = f2bf(__fdiv_rn(__fmaf_rn(acc[k], 1.0f, 0.0f), __fmaf_rn(sL[g], 1.0f, 0.0f)));
-        }
-        return;
-    }
-    float* wsb = a.ws + (static_cast<int64_t>(col) * a.hkv + kvh) * a.max_chunks * G * (HD + 2);
-    float* ws = wsb + static_cast<int64_t>(c) * G * (HD + 2);
-#pragma unroll
-    for (int k = 0; k < GPT; ++k) {
-        const int g = g0 + k * gstep;
-        if (g < G) ws[g * (HD + 2) + 2 + d] = acc[k];
-    }
-    if (tid < G) {
-        ws[tid * (HD + 2)] = sM[tid];
-        ws[tid * (HD + 2) + 1] = sL[tid];
-    }
-    // The last chunk CTA of this (column, kv head) combines all chunks in chunk order. The ticket only
-    // elects the combiner; every value is combined in the same fixed order whoever arrives last.
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        int* t = a.tickets + static_cast<int64_t>(col) * a.hkv + kvh;
-        const int prev = atomicAdd(t, 1);
-        s_last = prev == nch - 1;
-        if (s_last) *t = 0;   // ready for the next launch
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // out_d = bf16( (sum_c o_cd * a_c) / (sum_c l_c * a_c) ), a_c = exp(m_c - max_c m_c)
-    const int64_t cstride = static_cast<int64_t>(G) * (HD + 2);
-#pragma unroll
-    for (int k = 0; k < GPT; ++k) {
-        const int g = g0 + k * gstep;
-        if (g >= G) continue;
-        const float* base = wsb + g * (HD + 2);
-        float M = -FLT_MAX;
-        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(base + cc * cstride));
-        float L = 0.0f, O = 0.0f;
-        for (int cc = 0; cc < nch; ++cc) {
-            const float* w = base + cc * cstride;
-            const float al = det_expf(__fsub_rn(__ldcg(w), M));
-            L = __fmaf_rn(__ldcg(w + 1), al, L);
-            O = __fmaf_rn(__ldcg(w + 2 + d), al, O);
-        }
-        outp[g * HD + d] = f2bf(__fdiv_rn(O, L));
-    }
-}
-
-#endif
 
 // ------------------------------------------------------------------ softmax + decode
 // reference: det_softmax (detcore.cpp:187-198), decode_with_draw / decode_step (detcore.cpp:202-262)
@@ -694,6 +500,7 @@ __device__ __forceinline__ void sample_fail_nonfinite(const SampleParams& sp, in
 
 __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
     __shared__ SampleSmem sm;
+    const ExpTab tab = exp_tab_lane();   // before the dependency wait: off the critical path
     pdl_wait();
     pdl_trigger();
     const int r = blockIdx.x;
@@ -748,7 +555,6 @@ __global__ void __launch_bounds__(1024) sample_kernel(const SampleParams sp) {
     }
 
     // pass 2: e_i = exp(l_i - max); S = canonical tree of e
-    const ExpTab tab = exp_tab_lane();
     const float S = block_tree_sum_1024_fm(
         V, [&](int i, bool ok) { return ok ? L[i] : 0.0f; },
         [&](int i, bool ok, float l) {
@@ -817,6 +623,7 @@ __global__ void __launch_bounds__(256) sample_max_kernel(const SampleParams sp) 
 __global__ void __launch_bounds__(1024) sample_multi_kernel(const SampleParams sp) {
     __shared__ SampleSmem sm;
     __shared__ int s_last;
+    const ExpTab tab = exp_tab_lane();   // before the dependency wait: off the critical path
     pdl_wait();
     pdl_trigger();
     const int b = blockIdx.x, r = blockIdx.y, nblk = gridDim.x;
@@ -855,7 +662,6 @@ __global__ void __launch_bounds__(1024) sample_multi_kernel(const SampleParams s
         return;
     }
 
-    const ExpTab tab = exp_tab_lane();
     const int i0 = b * kSampleBlock;
     const int nloc = max(0, min(kSampleBlock, V - i0));
     const float part = block_tree_sum_1024_fm(
