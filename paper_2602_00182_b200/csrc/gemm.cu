@@ -104,6 +104,19 @@ __device__ __forceinline__ void epilogue_swiglu(const GemmParams& p, int row, in
     p.act[static_cast<int64_t>(col) * (p.n_out / 2) + (row >> 1)] = f2bf(__fmul_rn(sg, partner));
 }
 
+// SwiGLU of two adjacent columns at once: the even lane (gate row) finishes column c, the odd lane
+// (up row) column c + 1, so every lane evaluates one exp / division instead of both lanes of a pair
+// evaluating one. Same scalar arithmetic per output as epilogue_swiglu.
+__device__ __forceinline__ void epilogue_swiglu_pair(const GemmParams& p, int row, int col, float v0, float v1,
+                                                     ExpTab tab) {
+    const bool odd = (row & 1) != 0;
+    const float recv = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
+    const float g = odd ? recv : v0, u = odd ? v1 : recv;
+    const float e = det_expf_shfl(-g, tab);
+    const float sg = __fdiv_rn(g, __fadd_rn(1.0f, e));
+    p.act[static_cast<int64_t>(col + (odd ? 1 : 0)) * (p.n_out / 2) + (row >> 1)] = f2bf(__fmul_rn(sg, u));
+}
+
 __device__ __forceinline__ float epilogue_any(const GemmParams& p, int row, int col, float v, ExpTab tab) {
     if (p.mode == kEpiQkvRope || p.mode == kEpiSwiglu) {
         const float partner = __shfl_xor_sync(0xffffffffu, v, 1);   // callers keep `col` warp-uniform
@@ -613,16 +626,25 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
 #pragma unroll
                 for (int u = 0; u < QB; ++u) {
                     const int q = q0 + u * S;
+                    float sum[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float t[8];
+#pragma unroll
+                        for (int s = 0; s < 8; ++s)
+                            t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
+                        sum[e] = local_tree_sum<8>(t);
+                    }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int cl = q * 4 + e;
-                        if (q < nq && cl < ncols) {
-                            float t[8];
-#pragma unroll
-                            for (int s = 0; s < 8; ++s)
-                                t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
-                            epilogue_any(p, m0 + rl, col0 + cl, local_tree_sum<8>(t), tab);   // ss_out: <= 8 cols
+                        if (q >= nq || cl >= ncols) continue;   // warp-uniform
+                        if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
+                            epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
+                            ++e;   // both columns done
+                            continue;
                         }
+                        epilogue_any(p, m0 + rl, col0 + cl, sum[e], tab);   // ss_out: <= 8 cols
                     }
                 }
             }
