@@ -96,6 +96,39 @@ __device__ __forceinline__ void epilogue_qkv(const GemmParams& p, int row, int c
     (is_k ? p.kcache : p.vcache)[off] = b;
 }
 
+// The same epilogue with the row's and the column's parts computed once (many columns): a thread's
+// row is fixed, and each column's position and KV-cache destination come from shared memory.
+struct QkvRow {
+    int d;           // dimension within the head
+    bool rope;       // q or k row
+    int dst;         // 0 q_out, 1 kcache, 2 vcache
+    int64_t off;     // q: row; k/v: kvh * page * hd + d
+};
+__device__ __forceinline__ QkvRow qkv_row(const GemmParams& p, int row) {
+    const int qrows = p.hq * p.hd, krows = p.hkv * p.hd;
+    QkvRow r;
+    r.d = row % p.hd;
+    r.rope = row < qrows + krows;
+    r.dst = row < qrows ? 0 : r.rope ? 1 : 2;
+    const int kvh = r.dst == 0 ? 0 : (row - (r.dst == 1 ? qrows : qrows + krows)) / p.hd;
+    r.off = r.dst == 0 ? row : static_cast<int64_t>(kvh) * p.page * p.hd + r.d;
+    return r;
+}
+// kvbase = ((page_id * hkv) * page + pos % page) * hd for the column's position
+__device__ __forceinline__ void epilogue_qkv_col(const GemmParams& p, const QkvRow& r, int col, int pos,
+                                                 int64_t kvbase, float v, float partner) {
+    if (pos < 0) return;
+    if (r.rope) {
+        const int64_t i = static_cast<int64_t>(pos) * (p.hd / 2) + (r.d >> 1);
+        const float c = p.rope_cos[i], s = p.rope_sin[i];
+        if ((r.d & 1) == 0) v = __fsub_rn(__fmul_rn(v, c), __fmul_rn(partner, s));
+        else v = __fadd_rn(__fmul_rn(partner, s), __fmul_rn(v, c));
+    }
+    const __nv_bfloat16 b = f2bf(v);
+    if (r.dst == 0) p.q_out[static_cast<int64_t>(col) * (p.hq * p.hd) + r.off] = b;
+    else (r.dst == 1 ? p.kcache : p.vcache)[kvbase + r.off] = b;
+}
+
 // silu(g) * u with g = gate row 2j, u = up row 2j+1; silu(g) = g / (1 + exp(-g)).
 __device__ __forceinline__ void epilogue_swiglu(const GemmParams& p, int row, int col, float v, float partner,
                                                 float e /* det_expf(-v) */) {
@@ -371,6 +404,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(recv_bar + 1);
 
     __shared__ float s_red[4];
+    __shared__ int s_cpos[NSUB * SUB_N];        // QKV, many columns: each column's position ...
+    __shared__ int64_t s_ckv[NSUB * SUB_N];     // ... and KV-cache row base (epilogue_qkv_col)
     __shared__ uint64_t s_tm[kTraceMarks];   // timeline marks (p.trace only)
     const bool tracing = p.trace != nullptr;
     if (tracing && threadIdx.x < kTraceMarks) s_tm[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : 0;
@@ -516,6 +551,15 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         const ExpTab tab = exp_tab_lane();
         if (fused) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
         if (tracing && threadIdx.x == 128) s_tm[2] = globaltimer_ns();   // B operand built (fused)
+        if (p.mode == kEpiQkvRope && ncols > 8 && S > 1 && !push)   // read after the cluster barrier
+            for (int c = rl; c < ncols; c += 128) {
+                const int pos = p.col_pos[col0 + c];
+                s_cpos[c] = pos;
+                s_ckv[c] = pos < 0 ? 0
+                                   : ((static_cast<int64_t>(p.block_table[static_cast<int64_t>(p.col_req[col0 + c]) *
+                                                                               p.max_pages + pos / p.page]) * p.hkv) *
+                                          p.page + pos % p.page) * p.hd;
+            }
         EpiPre pre{0.0f, 0.0f, -1, 0};   // the first owned column's epilogue operands (decode)
         if (push && seg < ncols) pre = epilogue_preload(p, m0 + rl, col0 + seg);
         mbar_wait(tfull, 0);
@@ -600,6 +644,7 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
             // their DSMEM loads are in flight together.
             constexpr int QB = NSUB <= 2 ? 1 : 2;
             const int nq = ncols <= 8 ? 0 : (ncols + 3) >> 2;
+            const QkvRow qr = qkv_row(p, m0 + rl);
             for (int cl = seg; warp >= 4 && ncols <= 8 && cl < ncols; cl += S) {   // one column per CTA
                 float v[8];
 #pragma unroll
@@ -639,6 +684,11 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                     for (int e = 0; e < 4; ++e) {
                         const int cl = q * 4 + e;
                         if (q >= nq || cl >= ncols) continue;   // warp-uniform
+                        if (p.mode == kEpiQkvRope) {
+                            const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
+                            epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
+                            continue;
+                        }
                         if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
                             epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
                             ++e;   // both columns done
