@@ -680,6 +680,18 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                             t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
                         sum[e] = local_tree_sum<8>(t);
                     }
+                    if (p.mode == kEpiAddF32) {   // residual add: the quad's four loads first
+                        float res[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            res[e] = q < nq && q * 4 + e < ncols
+                                         ? p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] : 0.0f;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (q < nq && q * 4 + e < ncols)
+                                p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] = __fadd_rn(res[e], sum[e]);
+                        continue;
+                    }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int cl = q * 4 + e;
