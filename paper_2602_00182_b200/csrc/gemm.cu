@@ -384,6 +384,69 @@ __device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready,
 // runs its segment as one tcgen05 accumulation chain in TMEM; the S partial tiles are exchanged
 // through distributed shared memory and combined per element with the reference tree over the S
 // partials in segment order (detcore.cpp:135-150). S depends only on the GEMM shape.
+// Cluster combine of the S_ K-segment partial tiles (> 8 columns) and the epilogue: CTA `seg`
+// finalises column quads seg, seg + S_, ...; warp group wg takes every other round of QB_ quads.
+// Per element the reference tree over the S_ partials in segment order (local_tree_sum<8>, -0
+// padded: the padding adds are exact and compile away for a constant S_).
+template <int S_, int QB_>
+__device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbase, int seg, int wg, int nq, int ncols,
+                                              int m0, int rl, int col0, const QkvRow& qr, const int* s_cpos,
+                                              const int64_t* s_ckv, ExpTab tab) {
+    for (int q0 = seg + wg * QB_ * S_; q0 < nq; q0 += 2 * QB_ * S_) {
+        float4 v[QB_][S_];
+#pragma unroll
+        for (int u = 0; u < QB_; ++u) {
+            const int q = q0 + u * S_;
+#pragma unroll
+            for (int s = 0; s < S_; ++s)
+                v[u][s] = q < nq ? ld_dsmem_f32x4(mapa_shared(pbase + 16u * static_cast<uint32_t>(q * BM + rl), s))
+                                 : make_float4(kNegZero, kNegZero, kNegZero, kNegZero);
+        }
+#pragma unroll
+        for (int u = 0; u < QB_; ++u) {
+            const int q = q0 + u * S_;
+            float sum[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float t[8];
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    t[s] = s >= S_ ? kNegZero
+                         : e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
+                sum[e] = local_tree_sum<8>(t);
+            }
+            if (p.mode == kEpiAddF32) {   // residual add: the quad's four loads first
+                float res[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    res[e] = q < nq && q * 4 + e < ncols
+                                 ? p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] : 0.0f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (q < nq && q * 4 + e < ncols)
+                        p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] = __fadd_rn(res[e], sum[e]);
+                continue;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int cl = q * 4 + e;
+                if (q >= nq || cl >= ncols) continue;   // warp-uniform
+                if (p.mode == kEpiQkvRope) {
+                    const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
+                    epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
+                    continue;
+                }
+                if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
+                    epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
+                    ++e;   // both columns done
+                    continue;
+                }
+                epilogue_any(p, m0 + rl, col0 + cl, sum[e], tab);   // ss_out: <= 8 cols
+            }
+        }
+    }
+}
+
 template <int NSUB>
 __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -657,58 +720,14 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
                 const float xn = epilogue_any(p, m0 + rl, col0 + cl, sum, tab);
                 if (p.ss_out != nullptr) tile_sumsq(p, tile, col0 + cl, xn, warp - 4, lane, s_red);
             }
-            for (int q0 = seg + wg * QB * S; q0 < nq; q0 += 2 * QB * S) {
-                float4 v[QB][8];
-#pragma unroll
-                for (int u = 0; u < QB; ++u) {
-                    const int q = q0 + u * S;
-#pragma unroll
-                    for (int s = 0; s < 8; ++s)
-                        v[u][s] = (s < S && q < nq)
-                                      ? ld_dsmem_f32x4(mapa_shared(pbase + 16u * static_cast<uint32_t>(q * BM + rl), s))
-                                      : make_float4(kNegZero, kNegZero, kNegZero, kNegZero);
-                }
-#pragma unroll
-                for (int u = 0; u < QB; ++u) {
-                    const int q = q0 + u * S;
-                    float sum[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        float t[8];
-#pragma unroll
-                        for (int s = 0; s < 8; ++s)
-                            t[s] = e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
-                        sum[e] = local_tree_sum<8>(t);
-                    }
-                    if (p.mode == kEpiAddF32) {   // residual add: the quad's four loads first
-                        float res[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            res[e] = q < nq && q * 4 + e < ncols
-                                         ? p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] : 0.0f;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (q < nq && q * 4 + e < ncols)
-                                p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] = __fadd_rn(res[e], sum[e]);
-                        continue;
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int cl = q * 4 + e;
-                        if (q >= nq || cl >= ncols) continue;   // warp-uniform
-                        if (p.mode == kEpiQkvRope) {
-                            const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
-                            epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
-                            continue;
-                        }
-                        if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
-                            epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
-                            ++e;   // both columns done
-                            continue;
-                        }
-                        epilogue_any(p, m0 + rl, col0 + cl, sum[e], tab);   // ss_out: <= 8 cols
-                    }
-                }
+            switch (S) {
+                case 2: combine_quads<2, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 3: combine_quads<3, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 4: combine_quads<4, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 5: combine_quads<5, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 6: combine_quads<6, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 7: combine_quads<7, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                default: combine_quads<8, QB>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
             }
         }
         if (tracing && threadIdx.x == 128) s_tm[7] = globaltimer_ns();   // combine + epilogue done
