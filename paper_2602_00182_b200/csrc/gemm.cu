@@ -431,6 +431,10 @@ __device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbas
             for (int e = 0; e < 4; ++e) {
                 const int cl = q * 4 + e;
                 if (q >= nq || cl >= ncols) continue;   // warp-uniform
+                if (p.mode == kEpiStoreF32) {
+                    if (s_ckv[cl] >= 0) p.out[s_ckv[cl] + m0 + rl] = sum[e];
+                    continue;
+                }
                 if (p.mode == kEpiQkvRope) {
                     const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
                     epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
@@ -468,7 +472,8 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
 
     __shared__ float s_red[4];
     __shared__ int s_cpos[NSUB * SUB_N];        // QKV, many columns: each column's position ...
-    __shared__ int64_t s_ckv[NSUB * SUB_N];     // ... and KV-cache row base (epilogue_qkv_col)
+    __shared__ int64_t s_ckv[NSUB * SUB_N];     // ... and KV-cache row base (epilogue_qkv_col); f32
+                                                // store: the column's output base (-1: inactive)
     __shared__ uint64_t s_tm[kTraceMarks];   // timeline marks (p.trace only)
     const bool tracing = p.trace != nullptr;
     if (tracing && threadIdx.x < kTraceMarks) s_tm[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : 0;
@@ -614,6 +619,17 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         const ExpTab tab = exp_tab_lane();
         if (fused) norm_b_setup(p, bc, bready, kb0, nkb, col0, ncols, ew, lane);
         if (tracing && threadIdx.x == 128) s_tm[2] = globaltimer_ns();   // B operand built (fused)
+        if (p.mode == kEpiStoreF32 && ncols > 8 && S > 1 && !push)   // each column's output base (or -1)
+            for (int c = rl; c < ncols; c += 128) {
+                int64_t off = static_cast<int64_t>(col0 + c) * p.ld_out;
+                if (p.col_step != nullptr) {
+                    const int st = p.col_step[col0 + c];
+                    off = st < 0 ? -1
+                                 : static_cast<int64_t>(p.col_slot[col0 + c]) * p.slot_stride +
+                                       static_cast<int64_t>(st) * p.n_out;
+                }
+                s_ckv[c] = off;
+            }
         if (p.mode == kEpiQkvRope && ncols > 8 && S > 1 && !push)   // read after the cluster barrier
             for (int c = rl; c < ncols; c += 128) {
                 const int pos = p.col_pos[col0 + c];
