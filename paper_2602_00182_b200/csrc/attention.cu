@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
         cp_async_commit();
         for (int i = tid; i < (q1 - q0) * G * HD; i += kNT) {
             const int q = q0 + i / (G * HD), rem = i % (G * HD);
-            sQ[q * G * HD + rem] = bf2f(a.q[static_cast<int64_t>(col0 + q) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD + rem]);
+            sQ[q * G * HD + qperm(rem)] = bf2f(a.q[static_cast<int64_t>(col0 + q) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD + rem]);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -495,19 +495,11 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
-                const float kf[8] = {__uint_as_float(kv.x << 16), __uint_as_float(kv.x & 0xffff0000u),
-                                     __uint_as_float(kv.y << 16), __uint_as_float(kv.y & 0xffff0000u),
-                                     __uint_as_float(kv.z << 16), __uint_as_float(kv.z & 0xffff0000u),
-                                     __uint_as_float(kv.w << 16), __uint_as_float(kv.w & 0xffff0000u)};
 #pragma unroll
                 for (int k = 0; k < SR; ++k) {
                     const int r = rg + k * (kNT / CH);
-                    const float4* q4 = reinterpret_cast<const float4*>(sQ + r * HD + v * 8);
-                    const float4 qa = q4[0], qb = q4[1];
-                    float pr[8] = {__fmul_rn(qa.x, kf[0]), __fmul_rn(qa.y, kf[1]), __fmul_rn(qa.z, kf[2]),
-                                   __fmul_rn(qa.w, kf[3]), __fmul_rn(qb.x, kf[4]), __fmul_rn(qb.y, kf[5]),
-                                   __fmul_rn(qb.z, kf[6]), __fmul_rn(qb.w, kf[7])};
-                    float carry = local_tree_sum<8>(pr);
+                    float carry = qk_block8(kv, *reinterpret_cast<const ulonglong2*>(sQ + r * HD + v * 8),
+                                            *reinterpret_cast<const ulonglong2*>(sQ + r * HD + v * 8 + 4));
                     int lvl = 0;
 #pragma unroll
                     for (int b = v; b & 1; b >>= 1, ++lvl) carry = __fadd_rn(stk[k][lvl], carry);
