@@ -139,6 +139,8 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *                 columns (default 8), in the workspace/ticket path above (0: always cluster)
  *   "attn_stream_min_cols" decode attention from this many columns on runs the streamed kernel
  *                 (persistent CTAs, TMA ring of K/V chunks; default 9; 0: never)
+ *   "fuse_max_cols" decode RMSNorm folded into the consuming GEMMs up to this many columns
+ *                 (default and maximum 8; 0: separate RMSNorm kernels)
  *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor

@@ -123,6 +123,7 @@ struct Engine {
     int self_pf_kb = 8;   // GemmParams::self_pf_kb
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
+    int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
     int attn_stream_min_cols = 9;    // AttnParams::stream_min_cols (0: off)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
@@ -337,7 +338,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         return cudaErrorInvalidValue;
     // Decode with <= 8 columns: RMSNorm is fused into the consuming GEMMs (QKV, gate/up, lm_head),
     // which build their B operand from the f32 residual stream; bits are identical.
-    const bool fuse = final_all && ncols <= 8;
+    const bool fuse = final_all && ncols <= E->fuse_max_cols;
     e = launch_embed(E->embed, tok, E->x, fuse ? E->norm_ss : nullptr, E->layers[0].attn_norm, E->h, ncols, d, c.eps, s,
                      pdl);
     if (e != cudaSuccess) return e;
@@ -577,7 +578,7 @@ int get_graph(Engine* E, int ncols, cudaGraphExec_t* out) {
     ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
     uint64_t n = 0;
     cudaError_t e = forward(E, ncols, E->d_tok, E->d_pos, E->d_req, true, 0, &n);
-    if (e == cudaSuccess) e = head_and_sample(E, E->h, ncols, &n, ncols <= 8);
+    if (e == cudaSuccess) e = head_and_sample(E, E->h, ncols, &n, ncols <= E->fuse_max_cols);
     cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
     ENG_CUDA(e);
     ENG_CUDA(e2);
@@ -1230,7 +1231,7 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
         E->prof = &trail;
         mark(E, -1);
         err = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
-        if (err == cudaSuccess) err = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, ncols <= 8);
+        if (err == cudaSuccess) err = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, static_cast<int>(ncols) <= E->fuse_max_cols);
         E->prof = nullptr;
         if (err == cudaSuccess) err = cudaStreamSynchronize(E->stream);
         for (size_t i = 1; i < trail.size() && err == cudaSuccess; ++i) {
@@ -1269,6 +1270,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_stream_min_cols") == 0) E->attn_stream_min_cols = static_cast<int>(value);
+    else if (std::strcmp(name, "fuse_max_cols") == 0) E->fuse_max_cols = static_cast<int>(value < 0 ? 0 : value > 8 ? 8 : value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
         if (E->trace_buf != nullptr) cudaFree(E->trace_buf);
@@ -1325,7 +1327,7 @@ int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_
     cudaGraph_t g;
     ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = forward(E, static_cast<int>(ncols), E->d_tok, E->d_pos, E->d_req, true, 0, nullptr);
-    if (e == cudaSuccess) e = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, ncols <= 8);
+    if (e == cudaSuccess) e = head_and_sample(E, E->h, static_cast<int>(ncols), nullptr, static_cast<int>(ncols) <= E->fuse_max_cols);
     cudaError_t e2 = cudaStreamEndCapture(E->stream, &g);
     E->skip_mask = 0;
     ENG_CUDA(e);
