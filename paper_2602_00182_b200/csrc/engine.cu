@@ -120,7 +120,7 @@ struct Engine {
     // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
     // Default: the o-projection warms the first 16 MB of gate/up (tools/l2pf_scan.py).
     unsigned l2pf_mask = 2;
-    int self_pf_kb = 8;   // GemmParams::self_pf_kb
+    int self_pf_kb = 4;   // GemmParams::self_pf_kb (tools/l2pf_scan.py: 4 beat 8 by ~1 % at batch 1 and 8)
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
