@@ -539,39 +539,52 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
             }
         }
         __syncthreads();
-        {   // PV: dimension d, rows rb, rb + kNT/HD, ...: one V element feeds PR chains
-            const int d = tid % HD, rb = tid / HD;
-            const uint16_t* v16 = reinterpret_cast<const uint16_t*>(sV);
-            float acc[PR];
-            int nr[PR];
+        {   // PV: two dimensions x RPT consecutive rows per thread: one 4-byte V load feeds 2 * RPT chains
+            constexpr int TPR = HD / 2;             // threads per row group
+            constexpr int RPT = R * TPR / kNT;      // rows per thread (PR / 2)
+            static_assert(2 * RPT == PR && kNT % TPR == 0, "PV mapping");
+            const int d0 = (tid % TPR) * 2, r0 = (tid / TPR) * RPT;   // r0 warp-uniform
+            const uint32_t* v32 = reinterpret_cast<const uint32_t*>(sV);
+            float acc[RPT][2];
+            int nr[RPT];
             int nmin = CH;
 #pragma unroll
-            for (int k = 0; k < PR; ++k) {
-                acc[k] = 0.0f;
-                nr[k] = s_run[(rb + k * (kNT / HD)) / G];
+            for (int k = 0; k < RPT; ++k) {
+                acc[k][0] = acc[k][1] = 0.0f;
+                nr[k] = s_run[(r0 + k) / G];
                 nmin = min(nmin, nr[k]);
             }
-            const float* srow = sS + rb * CH;   // row rb + k*(kNT/HD) at srow + k*(kNT/HD)*CH
+            const float* srow = sS + r0 * CH;   // row r0 + k at srow + k*CH
 #pragma unroll 4
             for (int p = 0; p < nmin; ++p) {   // every row active: no per-FMA guard
-                const float v = __uint_as_float(static_cast<uint32_t>(v16[p * HD + d]) << 16);
+                const uint32_t w = v32[(p * HD + d0) >> 1];
+                const float v0 = __uint_as_float(w << 16), v1 = __uint_as_float(w & 0xffff0000u);
 #pragma unroll
-                for (int k = 0; k < PR; ++k) acc[k] = __fmaf_rn(srow[k * (kNT / HD) * CH + p], v, acc[k]);
+                for (int k = 0; k < RPT; ++k) {
+                    const float e = srow[k * CH + p];
+                    acc[k][0] = __fmaf_rn(e, v0, acc[k][0]);
+                    acc[k][1] = __fmaf_rn(e, v1, acc[k][1]);
+                }
             }
             for (int p = nmin; p < nmax; ++p) {   // the causal edge
-                const float v = __uint_as_float(static_cast<uint32_t>(v16[p * HD + d]) << 16);
+                const uint32_t w = v32[(p * HD + d0) >> 1];
+                const float v0 = __uint_as_float(w << 16), v1 = __uint_as_float(w & 0xffff0000u);
 #pragma unroll
-                for (int k = 0; k < PR; ++k)
-                    if (p < nr[k]) acc[k] = __fmaf_rn(srow[k * (kNT / HD) * CH + p], v, acc[k]);
+                for (int k = 0; k < RPT; ++k)
+                    if (p < nr[k]) {
+                        const float e = srow[k * CH + p];
+                        acc[k][0] = __fmaf_rn(e, v0, acc[k][0]);
+                        acc[k][1] = __fmaf_rn(e, v1, acc[k][1]);
+                    }
             }
 #pragma unroll
-            for (int k = 0; k < PR; ++k) {
-                const int r = rb + k * (kNT / HD), q = r / G, g = r % G;
+            for (int k = 0; k < RPT; ++k) {
+                const int r = r0 + k, q = r / G, g = r % G;
                 if (nr[k] == 0) continue;
                 float* ws = a.ws + ((static_cast<int64_t>(col0 + q) * a.hkv + kvh) * a.max_chunks + c) * G * (HD + 4) +
                             g * (HD + 4);
-                ws[4 + d] = acc[k];
-                if (d == 0) {
+                *reinterpret_cast<float2*>(ws + 4 + d0) = make_float2(acc[k][0], acc[k][1]);
+                if (d0 == 0) {
                     ws[0] = sM[r];
                     ws[1] = sL[r];
                 }
