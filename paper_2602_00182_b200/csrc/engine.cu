@@ -14,6 +14,7 @@
 #include <memory>
 #include <string>
 #include <future>
+#include <deque>
 #include <thread>
 #include <vector>
 
@@ -104,7 +105,8 @@ struct Engine {
         size_t cap = 0;
         std::shared_future<void> busy;
     };
-    std::vector<HashBuf> hash_bufs;
+    std::deque<HashBuf> hash_bufs;   // deque: growing it never moves a buffer in use
+    size_t hash_next = 0;            // round-robin victim when every buffer is busy
     // decode graphs keyed by (ncols, slot_stride)
     std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
     uint64_t launches_per_step = 0;
@@ -759,18 +761,24 @@ int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* l
         Timer tw;
         float* dst = logits_out;
         Engine::HashBuf* hb = nullptr;
-        if (dst == nullptr) {   // a pinned buffer whose previous hash is done (at most three)
+        if (dst == nullptr) {
+            // a pinned buffer whose previous hash is done; the pool grows to one buffer per spare
+            // host thread (3..16), so many requests finishing together hash in parallel; when all
+            // are busy, wait for the oldest
+            static const size_t kMaxBufs = std::max<size_t>(3, std::min<size_t>(16, std::thread::hardware_concurrency() > 2
+                                                                                         ? std::thread::hardware_concurrency() - 2
+                                                                                         : 3));
             for (auto& b : E->hash_bufs)
                 if (!b.busy.valid() || b.busy.wait_for(std::chrono::seconds(0)) == std::future_status::ready) {
                     hb = &b;
                     break;
                 }
-            if (hb == nullptr && E->hash_bufs.size() < 3) {
+            if (hb == nullptr && E->hash_bufs.size() < kMaxBufs) {
                 E->hash_bufs.emplace_back();
                 hb = &E->hash_bufs.back();
             }
             if (hb == nullptr) {
-                hb = &E->hash_bufs.front();
+                hb = &E->hash_bufs[E->hash_next++ % E->hash_bufs.size()];
                 hb->busy.wait();
             }
             if (hb->cap < n) {
