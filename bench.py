@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--gen", type=int, default=256)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
+    ap.add_argument("--sweep", default="auto", choices=["auto", "off"],
+                    help="N=1: decode-step tok/s and step roofline at batch 1/8/64/256 (context 640)")
     ap.add_argument("--cpu-sample-prompt", type=int, default=4)
     ap.add_argument("--cpu-sample-gen", type=int, default=2)
     return ap.parse_args()
@@ -115,6 +117,33 @@ def step_bytes(info, batch: int, prompt: int, gen: int) -> float:
     mean_ctx = prompt + gen / 2.0
     per_req = kv_per_pos * mean_ctx + kv_per_pos + 2 * d + 4 * V
     return weights + batch * per_req
+
+
+def batch_sweep(model: str, eng_b1, batches=(1, 8, 64, 256), ctx: int = 640):
+    """Decode-step throughput vs batch (config 3's batch sizes) on a second engine with 256 slots:
+    CUDA-graph step time with every column at context `ctx` (detgpu_profile_graph), tok/s and the
+    step's HBM roofline fraction (SURVEY.md §8(d) bytes). Receipt identity across these batch sizes
+    is tests/test_gpu_determinism.py's job; this is throughput only."""
+    import ctypes as C
+
+    from paper_2602_00182_b200 import _lib as L
+    from paper_2602_00182_b200.detcore import Engine
+
+    info = eng_b1.info
+    peak, _ = peaks()
+    eng = Engine(model, "b200", max_batch=max(batches), max_context=max(ctx + 1, 768))
+    out = {"ctx": ctx, "what": "CUDA-graph decode step, every column at context ctx; step_frac = SURVEY §8(d) bytes "
+                              "/ step time / measured HBM peak"}
+    try:
+        for b in batches:
+            ms = C.c_float()
+            L.check(L.lib.detgpu_profile_graph(eng.h, b, ctx, 0, 10, C.byref(ms)), eng.h)
+            sb = step_bytes(info, b, ctx, 0)
+            out[str(b)] = {"ms_per_step": round(ms.value, 4), "tok_s": round(b / ms.value * 1e3, 1),
+                           "step_frac": round(sb / (ms.value / 1e3) / 1e9 / peak, 4)}
+    finally:
+        eng.close()
+    return out
 
 
 def cpu_oracle_sample(model: str, prompt_len: int, gen: int, vocab_hint: int = 128256):
@@ -282,6 +311,12 @@ def run_ours(args, rank: int, world: int, local: int):
 
     if rank != 0:
         return
+    sweep = None
+    if args.sweep == "auto" and world == 1:
+        try:
+            sweep = batch_sweep(args.model, eng)
+        except Exception as e:   # noqa: BLE001
+            sweep = {"unavailable": str(e)[:200]}
     cpu = None
     if args.cpu_baseline == "auto" and world == 1:
         try:
@@ -321,6 +356,7 @@ def run_ours(args, rank: int, world: int, local: int):
         "decode_tok_s": decode_tok_s, "prefill_ms": prefill_ms / args.steps,
         "replay_match_rate": replay_rate, "cross_gpu_receipts_equal": bool(cross_equal),
         "receipt_probe_out_hash": probe[0].hex(),
+        "decode_batch_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
 
