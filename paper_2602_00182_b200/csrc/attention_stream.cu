@@ -12,7 +12,8 @@
 //   are conflict-free), plus the column's q (1D bulk copy), completing on the stage's mbarrier;
 // * four consumer groups of 64 threads take the ring's chunks round robin: chunk j -> group j % 4.
 //   Each chunk's partial (m, l, o) goes to the workspace; the group that completes a (column, kv
-//   head)'s ticket combines it.
+//   head) combines it. Completion is counted per CTA in shared memory; only an item split between
+//   two CTAs' ranges (at most two per CTA) also goes through a global ticket.
 //
 // A chunk's bits do not depend on which CTA, group or stage computes it, and the combine order is
 // fixed, so the output is identical to attn_chunk_kernel's (tests/test_gpu_engine.py).
