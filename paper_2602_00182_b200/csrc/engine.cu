@@ -122,6 +122,8 @@ struct Engine {
     // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
     // Default: the o-projection warms the first 16 MB of gate/up (tools/l2pf_scan.py).
     unsigned l2pf_mask = 2;
+    int self_pf_kb_down = 0;   // the down GEMM's (-1: self_pf_kb): it launches during the gate/up tail,
+                               // where extra prefetch competes with gate/up's own stream (l2pf_scan: 0 best)
     int self_pf_kb = 4;   // GemmParams::self_pf_kb (tools/l2pf_scan.py: 4 beat 8 by ~1 % at batch 1 and 8)
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
@@ -454,6 +456,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         mark(E, kProfGateUp);
         GemmParams gd = gemm_base(E, Ly.wdown, d, c.F, ncols);
         gd.mode = kEpiAddF32;
+        if (E->self_pf_kb_down >= 0) gd.self_pf_kb = E->self_pf_kb_down;
         gd.trace_tag = kProfDown;
         gd.out = E->x;
         gd.ld_out = d;
@@ -1274,6 +1277,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "l2pf_cap_mb") == 0) E->l2pf_cap = value << 20;
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
+    else if (std::strcmp(name, "self_pf_kb_down") == 0) E->self_pf_kb_down = static_cast<int>(value);
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
