@@ -144,7 +144,8 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor
- *   "self_pf_kb_down" the same for the down projection alone (default 0; -1: self_pf_kb)
+ *   "self_pf_kb_qkv" / "_o" / "_gate_up" / "_down" / "_lm_head": the same for one GEMM class
+ *                 (-1: self_pf_kb; default -1 except the o and down projections: 0)
  *   "trace"       > 0: record a per-CTA timeline of the decode kernels (capacity in records), 0: off
  * Cached decode graphs are dropped. Returns DETGPU_EINVAL for an unknown name. */
 int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value);

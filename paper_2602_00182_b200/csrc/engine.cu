@@ -122,8 +122,10 @@ struct Engine {
     // bytes each. Scheduling only: results are unaffected. DETGPU_L2PF / DETGPU_L2PF_MB override.
     // Default: the o-projection warms the first 16 MB of gate/up (tools/l2pf_scan.py).
     unsigned l2pf_mask = 2;
-    int self_pf_kb_down = 0;   // the down GEMM's (-1: self_pf_kb): it launches during the gate/up tail,
-                               // where extra prefetch competes with gate/up's own stream (l2pf_scan: 0 best)
+    // per-GEMM overrides of self_pf_kb (-1: self_pf_kb), order qkv, o, gate/up, down, lm_head. The
+    // down GEMM launches during the gate/up tail, where its prefetch competes with gate/up's own
+    // stream; for o and down 0 measured best (tools/l2pf_scan.py, batch 1: -1.5 % and -0.4 %)
+    int self_pf_kb_cls[5] = {-1, 0, -1, 0, -1};
     int self_pf_kb = 4;   // GemmParams::self_pf_kb (tools/l2pf_scan.py: 4 beat 8 by ~1 % at batch 1 and 8)
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
@@ -351,6 +353,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
     for (int l = 0; l < c.L; ++l) {
         const Layer& Ly = E->layers[l];
         GemmParams g = gemm_base(E, Ly.wqkv, qd + 2 * kd, d, ncols);
+        if (E->self_pf_kb_cls[0] >= 0) g.self_pf_kb = E->self_pf_kb_cls[0];
         g.mode = kEpiQkvRope;
         g.trace_tag = kProfQkv;
         g.q_out = E->q;
@@ -416,6 +419,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         if (!(E->skip_mask & (1u << kProfAttn)) && (e = launch_attention(a, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfAttn);
         GemmParams go = gemm_base(E, Ly.wo, d, qd, ncols);
+        if (E->self_pf_kb_cls[1] >= 0) go.self_pf_kb = E->self_pf_kb_cls[1];
         go.mode = kEpiAddF32;
         go.trace_tag = kProfO;
         go.out = E->x;
@@ -438,6 +442,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
             ++n;
         }
         GemmParams gu = gemm_base(E, Ly.wgu, 2 * c.F, d, ncols);
+        if (E->self_pf_kb_cls[2] >= 0) gu.self_pf_kb = E->self_pf_kb_cls[2];
         gu.mode = kEpiSwiglu;
         gu.trace_tag = kProfGateUp;
         gu.act = E->act;
@@ -456,7 +461,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         mark(E, kProfGateUp);
         GemmParams gd = gemm_base(E, Ly.wdown, d, c.F, ncols);
         gd.mode = kEpiAddF32;
-        if (E->self_pf_kb_down >= 0) gd.self_pf_kb = E->self_pf_kb_down;
+        if (E->self_pf_kb_cls[3] >= 0) gd.self_pf_kb = E->self_pf_kb_cls[3];
         gd.trace_tag = kProfDown;
         gd.out = E->x;
         gd.ld_out = d;
@@ -504,6 +509,7 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
     CUtensorMap tmX;
     if (!make_tmap_bf16(&tmX, X, c.d, ncols, 64)) return cudaErrorInvalidValue;
     GemmParams g = gemm_base(E, E->lm_head, c.V, c.d, ncols);
+    if (E->self_pf_kb_cls[4] >= 0) g.self_pf_kb = E->self_pf_kb_cls[4];
     g.mode = kEpiStoreF32;
     g.trace_tag = kProfLmHead;
     if (fuse_norm) {   // final RMSNorm fused into the lm_head's B operand (decode, <= 8 columns)
@@ -1277,7 +1283,13 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "l2pf_cap_mb") == 0) E->l2pf_cap = value << 20;
     else if (std::strcmp(name, "pdl") == 0) E->use_pdl = value != 0;
     else if (std::strcmp(name, "self_pf_kb") == 0) E->self_pf_kb = static_cast<int>(value);
-    else if (std::strcmp(name, "self_pf_kb_down") == 0) E->self_pf_kb_down = static_cast<int>(value);
+    else if (std::strncmp(name, "self_pf_kb_", 11) == 0) {
+        static const char* kCls[5] = {"qkv", "o", "gate_up", "down", "lm_head"};
+        int i = 0;
+        while (i < 5 && std::strcmp(name + 11, kCls[i]) != 0) ++i;
+        if (i == 5) return fail(E, DETGPU_EINVAL, std::string("set_option: unknown option '") + name + "'");
+        E->self_pf_kb_cls[i] = static_cast<int>(value);
+    }
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
