@@ -466,6 +466,12 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
         s_n[tid] = pos >= p0 ? min(CH, pos + 1 - p0) : 0;
     }
     __syncthreads();
+    {   // causal prefill: about half the (chunk, query block) CTAs see no position of their chunk
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) any |= s_n[q] > 0;
+        if (!any) return;
+    }
     const ExpTab tab = exp_tab_lane();
     for (int q0 = 0; q0 < Q;) {   // runs of queries of one request share the K/V chunk
         int q1 = q0 + 1;
