@@ -238,3 +238,26 @@ def test_streamed_decode_attention_bit_exact(tiny_oracle):
         assert t[i].tolist() == ot.tolist(), i
         assert (l[i].view(np.uint32) == ol.view(np.uint32)).all(), i
     eng.close()
+
+
+def test_streamed_attention_items_spanning_many_ctas(tiny_oracle):
+    """Few columns with long contexts: a (column, kv head) item's chunks spread over many persistent
+    CTAs (global-ticket completion), and 32-chunk contexts; bit-identical to the cluster /
+    workspace kernels and, for one request, to the oracle."""
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    eng = Engine("llama-tiny:model-a", "b200", max_batch=4, max_context=2100)
+    lens = [2000, 1500, 700, 64]
+    prompts = [_prompt(900 + i, n, eng.vocab) for i, n in enumerate(lens)]
+    pols = [DecodePolicy.greedy(4)] * len(lens)
+    seeds = [3] * len(lens)
+    eng.set_option("attn_stream_min_cols", 0)
+    ref_t, ref_l, ref_h = eng.generate(prompts, pols, seeds, batch_size=len(lens))
+    for bs in (1, 4):
+        eng.set_option("attn_stream_min_cols", 1)
+        t, l, h = eng.generate(prompts, pols, seeds, batch_size=bs)
+        assert h == ref_h, bs
+    ot, ol = tiny_oracle.generate(prompts[0], max_tokens=4, seed=3)
+    assert t[0].tolist() == ot.tolist()
+    assert (l[0].view(np.uint32) == ol.view(np.uint32)).all()
+    eng.close()
