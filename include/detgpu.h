@@ -137,6 +137,8 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *                 one query per CTA (0)
  *   "attn_cluster_max_cols" decode attention combines chunks in a cluster up to this many
  *                 columns (default 8), in the workspace/ticket path above (0: always cluster)
+ *   "attn_sep_recv_max_cols" up to this many columns the cluster combine's leader receives the
+ *                 chunk partials in a buffer of its own (no push handshake; default 2, 0: never)
  *   "attn_stream_min_cols" decode attention from this many columns on runs the streamed kernel
  *                 (persistent CTAs, TMA ring of K/V chunks; default 9; 0: never)
  *   "fuse_max_cols" decode RMSNorm folded into the consuming GEMMs up to this many columns

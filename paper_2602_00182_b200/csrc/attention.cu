@@ -227,11 +227,20 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     if (threadIdx.x == 0)
         l2_prefetch_slice(a.l2pf, a.l2pf_bytes, c + gridDim.x * (kvh + gridDim.y * col),
                           gridDim.x * gridDim.y * gridDim.z);
+    // sep_recv: the leader's partial-receive buffer follows its K/V buffer, so pushes need no
+    // handshake; the leader arms its barrier for the pushed bytes before the cluster barrier
+    const bool sep = CL && a.sep_recv != 0;
     if constexpr (CL) {
         if (threadIdx.x == 0) {
             mbar_init(&s_bar[0], 1);
             mbar_init(&s_bar[1], 1);
             fence_mbar_init();
+            if (sep && c == 0) {
+                const int pos0 = a.col_pos[col];
+                const int nch0 = pos0 < 0 ? 0 : pos0 / kAttnChunk + 1;
+                if (nch0 > 1)
+                    mbar_arrive_expect_tx(&s_bar[0], static_cast<uint32_t>((nch0 - 1) * G * (HD + 2) * 4));
+            }
         }
         __syncthreads();
         cluster_arrive();   // every CTA of the cluster, active or not, arrives once and waits once
@@ -301,12 +310,14 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     if constexpr (CL) {
         if (nch > 1) {
             constexpr int BLK = G * (HD + 2);   // one pushed partial: m[G], l[G], o[G][HD]
-            float* recv = reinterpret_cast<float*>(attn_dsm);
+            float* recv = reinterpret_cast<float*>(attn_dsm + (sep ? 2 * CH * HD * 2 : 0));
             if (c == 0) {
-                __syncthreads();   // the leader's own K/V reads are complete
-                if (tid == 0) mbar_arrive_expect_tx(&s_bar[0], static_cast<uint32_t>((nch - 1) * BLK * 4));
+                if (!sep) {
+                    __syncthreads();   // the leader's own K/V reads are complete
+                    if (tid == 0) mbar_arrive_expect_tx(&s_bar[0], static_cast<uint32_t>((nch - 1) * BLK * 4));
+                }
                 cluster_wait();
-                if (tid >= 1 && tid < nch) mbar_arrive_remote(mapa_shared(smem_u32(&s_bar[1]), tid));
+                if (!sep && tid >= 1 && tid < nch) mbar_arrive_remote(mapa_shared(smem_u32(&s_bar[1]), tid));
                 if (tid < G) {
                     float M = sM[tid];   // chunk order: fmaxf chain from -FLT_MAX (see the ticket combine)
                     M = fmaxf(-FLT_MAX, M);
@@ -340,7 +351,7 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
                 }
             } else {
                 cluster_wait();
-                mbar_wait(&s_bar[1], 0);   // the leader no longer reads its K/V buffer
+                if (!sep) mbar_wait(&s_bar[1], 0);   // the leader no longer reads its K/V buffer
                 const uint32_t rb = mapa_shared(smem_u32(recv) + 4u * static_cast<uint32_t>((c - 1) * BLK), 0);
                 const uint32_t rbar = mapa_shared(smem_u32(&s_bar[0]), 0);
 #pragma unroll
@@ -401,12 +412,14 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
 
 template <int HD, int G, bool CL>
 cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
+    constexpr size_t dsm_kv = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
+    constexpr size_t dsm_max = dsm_kv + (CL ? static_cast<size_t>(kMaxClusterChunks - 1) * G * (HD + 2) * 4 : 0);
+    const size_t dsm = dsm_kv + (CL && a.sep_recv ? static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 : 0);
     static std::atomic<uint64_t> attr_devs{0};
     int dev = 0;
     if (attrs_needed(attr_devs, &dev)) {
         cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm_max));
         if (e == cudaSuccess && CL)
             e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;

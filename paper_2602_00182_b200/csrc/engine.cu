@@ -131,6 +131,7 @@ struct Engine {
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
     int attn_stream_min_cols = 9;    // AttnParams::stream_min_cols (0: off)
+    int attn_sep_recv_max_cols = 2;   // AttnParams::sep_recv up to this many columns (0: never)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
     int64_t l2pf_cap = 16ll << 20;
@@ -406,6 +407,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.decode = final_all ? 1 : 0;   // decode steps (final_all) vs prefill chunks
         a.prefill_blocks = E->prefill_blocks ? 1 : 0;
         a.cluster_max_cols = E->attn_cluster_max_cols;
+        a.sep_recv = ncols <= E->attn_sep_recv_max_cols ? 1 : 0;
         a.tm_k = &E->tm_kpool;
         a.tm_v = &E->tm_vpool;
         a.kv_row0 = static_cast<int64_t>(per_layer / c.hd) * l;
@@ -1293,6 +1295,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
+    else if (std::strcmp(name, "attn_sep_recv_max_cols") == 0) E->attn_sep_recv_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_stream_min_cols") == 0) E->attn_stream_min_cols = static_cast<int>(value);
     else if (std::strcmp(name, "fuse_max_cols") == 0) E->fuse_max_cols = static_cast<int>(value < 0 ? 0 : value > 8 ? 8 : value);
     else if (std::strcmp(name, "trace") == 0) {

@@ -53,6 +53,7 @@ struct AttnParams {
     int decode;                    // 1: every column's positions < pos were written by earlier launches
     int prefill_blocks;            // prefill: query blocks share each K/V chunk (attn_prefill_kernel)
     int cluster_max_cols;          // decode: cluster combine up to this many columns (0: always)
+    int sep_recv;                  // cluster combine: separate receive buffer (no push handshake)
     const void* l2pf;              // optional: bytes warmed into L2 at kernel start (the o weights)
     int64_t l2pf_bytes;
     TraceRec* trace;        // optional per-CTA timeline (timing instrumentation)
