@@ -144,6 +144,8 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *   "fuse_max_cols" decode RMSNorm folded into the consuming GEMMs up to this many columns
  *                 (default and maximum 8; 0: separate RMSNorm kernels)
  *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
+ *   "gemm_pair"   GEMMs above 64 columns as CTA pairs (tcgen05 cta_group::2, 256 x 128 tiles;
+ *                 bit-identical; default 0: measured no faster than two one-CTA tiles per SM)
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the
  *                 shared-memory ring into L2 before waiting on their predecessor
  *   "self_pf_kb_qkv" / "_o" / "_gate_up" / "_down" / "_lm_head": the same for one GEMM class
@@ -200,7 +202,8 @@ int detgpu_decode_exec_tuple(const uint8_t* bytes, size_t n, char* model_id, siz
 int detgpu_k_gemm(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy,
                   void* stream);
 /* Same with an explicit number of fixed K-segments (1..8; 0 = the engine's shape rule). Changes the
- * numeric definition: measurement hook only. */
+ * numeric definition: measurement hook only. Test hooks: -1 = the engine's rule with the wide-N MMA
+ * form; 200 + S = the CTA-pair (cta_group::2) kernel above 64 columns (same bits). */
 int detgpu_k_gemm_split(const void* W, const void* X, float* Y, int n_out, int K, int ncols, int64_t ldy,
                         int ksplit, void* stream);
 /* out[col][i] = bf16(x[col][i] * rstd * gamma[i]); x f32 [ncols,d]; canonical-tree sum of squares. */

@@ -52,6 +52,10 @@ int detgpu_k_gemm_split(const void* W, const void* X, float* Y, int n_out, int K
     p.out = Y;
     p.ld_out = ldy;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ksplit >= 200) {   // test hook: 200 + S (0: the shape rule) selects the CTA-pair kernel above 64 columns
+        p.pair = 1;
+        ksplit -= 200;
+    }
     p.ksplit = ksplit < 0 ? 0 : ksplit;
     p.mma_wide = ksplit < 0 ? 1 : 0;   // test hook: negative ksplit selects the wide-N MMA form
     DETGPU_CUDA_TRY(gemm_launch(tw, tx, p, s, true));

@@ -391,7 +391,7 @@ __device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready,
 template <int S_, int QB_>
 __device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbase, int seg, int wg, int nq, int ncols,
                                               int m0, int rl, int col0, const QkvRow& qr, const int* s_cpos,
-                                              const int64_t* s_ckv, ExpTab tab) {
+                                              const int64_t* s_ckv, ExpTab tab, int rstride = 1, int roff = 0) {
     for (int q0 = seg + wg * QB_ * S_; q0 < nq; q0 += 2 * QB_ * S_) {
         float4 v[QB_][S_];
 #pragma unroll
@@ -399,7 +399,8 @@ __device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbas
             const int q = q0 + u * S_;
 #pragma unroll
             for (int s = 0; s < S_; ++s)
-                v[u][s] = q < nq ? ld_dsmem_f32x4(mapa_shared(pbase + 16u * static_cast<uint32_t>(q * BM + rl), s))
+                v[u][s] = q < nq ? ld_dsmem_f32x4(mapa_shared(pbase + 16u * static_cast<uint32_t>(q * BM + rl),
+                                                              static_cast<uint32_t>(s * rstride + roff)))
                                  : make_float4(kNegZero, kNegZero, kNegZero, kNegZero);
         }
 #pragma unroll
@@ -760,6 +761,204 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
         trace_record(p.trace, (p.trace_tag << 24) | (blockIdx.x + S * (tile + ntiles * cgrp)), s_tm);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Many columns (> 64): CTA pairs (cta_group::2). A pair computes a 256-row x 128-column tile of one
+// K-segment chain: each CTA loads its 128 weight rows and 64 of the 128 activation columns per
+// k-block (24 KB instead of 32 KB for the same 128 x 128 x 64 MACs per SM, four stages in flight
+// instead of three), the even CTA issues one M = 256, N = 128 tcgen05.mma per K step, and each
+// CTA's TMEM holds its 128 rows x 128 columns. The S K-segments are S pairs of one cluster (rank
+// 2s + v) and are combined exactly as in gemm_tc_kernel (combine_quads over ranks 2s' + v), so
+// every output element has the same K order, chains and tree: the bits equal the one-CTA form
+// (tests/test_gpu_gemm.py).
+constexpr int kPairStages = 4;
+constexpr int kPairSmem = kPairStages * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+__global__ void __launch_bounds__(256, 2)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kPairStages * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kPairStages * B_BYTES);
+    uint64_t* empty = full + kPairStages;
+    uint64_t* tfull = empty + kPairStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    __shared__ int s_cpos[2 * SUB_N];
+    __shared__ int64_t s_ckv[2 * SUB_N];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = p.ksplit;
+    const int rank = static_cast<int>(blockIdx.x), v = rank & 1, seg = rank >> 1;
+    const uint32_t leader = static_cast<uint32_t>(rank & ~1);
+    const int m0 = static_cast<int>(blockIdx.z) * 2 * BM + v * BM, tile = m0 / BM;
+    const int col0 = static_cast<int>(blockIdx.y) * 2 * SUB_N;
+    const int ncols = min(2 * SUB_N, p.ncols - col0);
+    const int bcol = col0 + v * SUB_N;   // this CTA's half of the pair's B columns
+    const int nkb_all = p.k / BK;
+    const int kb0 = seg * nkb_all / S, nkb = (seg + 1) * nkb_all / S - kb0;
+    constexpr uint32_t kStageTx = 2 * (A_BYTES + B_BYTES);   // both CTAs' bytes land on the leader's barrier
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc_pair(tslot, 2 * SUB_N);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync_all();   // every pair member's barriers exist before any remote arrive / complete_tx
+    const uint32_t tbase = *tslot;
+
+    auto load_w = [&](int s, int kb) {
+        const uint32_t bar = mapa_shared(smem_u32(&full[s]), leader);
+        if (p.w_tiled) tma_load_3d_pair(sA + s * A_BYTES, &tmW, bar, 0, 0, tile * nkb_all + kb, kEvictFirst);
+        else tma_load_3d_pair(sA + s * A_BYTES, &tmW, bar, 0, kb, m0, kEvictFirst);
+    };
+    auto load_x = [&](int s, int kb) {
+        tma_load_2d_pair(sB + s * B_BYTES, &tmX, mapa_shared(smem_u32(&full[s]), leader), kb * BK, bcol, kEvictLast);
+    };
+    const int pre = min(kPairStages, nkb);
+    if (threadIdx.x == 0)   // weight tiles do not depend on the previous kernel
+        for (int i = 0; i < pre; ++i) {
+            if (v == 0) mbar_arrive_expect_tx(&full[i], kStageTx);
+            load_w(i, kb0 + i);
+        }
+    pdl_wait();
+    pdl_trigger();
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < pre; ++i) load_x(i, kb0 + i);
+            int s = pre % kPairStages, ph = (pre / kPairStages) & 1;
+            for (int i = pre; i < nkb; ++i) {
+                mbar_wait(&empty[s], ph ^ 1);
+                if (v == 0) mbar_arrive_expect_tx(&full[s], kStageTx);
+                load_w(s, kb0 + i);
+                load_x(s, kb0 + i);
+                if (++s == kPairStages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && v == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, 2 * SUB_N);
+            const uint16_t mask = static_cast<uint16_t>(3u << leader);
+            int s = 0, ph = 0;
+            for (int i = 0; i < nkb; ++i) {
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(sA + s * A_BYTES), b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                    tc_mma_bf16_pair(tbase, umma_desc_k128(a_base + k * 32), umma_desc_k128(b_base + k * 32), idesc,
+                                     (i | k) != 0 ? 1u : 0u);
+                tc_commit_pair_mc(&empty[s], mask);   // frees this stage in both pair members
+                if (++s == kPairStages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            tc_commit_pair_mc(tfull, mask);
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4, rl = ew * 32 + lane;
+        // per-column epilogue operands (read after the cluster barrier below)
+        if (p.mode == kEpiStoreF32)
+            for (int c = rl; c < ncols; c += 128) {
+                int64_t off = static_cast<int64_t>(col0 + c) * p.ld_out;
+                if (p.col_step != nullptr) {
+                    const int st = p.col_step[col0 + c];
+                    off = st < 0 ? -1
+                                 : static_cast<int64_t>(p.col_slot[col0 + c]) * p.slot_stride +
+                                       static_cast<int64_t>(st) * p.n_out;
+                }
+                s_ckv[c] = off;
+            }
+        if (p.mode == kEpiQkvRope)
+            for (int c = rl; c < ncols; c += 128) {
+                const int pos = p.col_pos[col0 + c];
+                s_cpos[c] = pos;
+                s_ckv[c] = pos < 0 ? 0
+                                   : ((static_cast<int64_t>(p.block_table[static_cast<int64_t>(p.col_req[col0 + c]) *
+                                                                               p.max_pages + pos / p.page]) * p.hkv) *
+                                          p.page + pos % p.page) * p.hd;
+            }
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        float4* P4 = reinterpret_cast<float4*>(smem);   // partial tile [column quad][row] (stages idle)
+#pragma unroll 1
+        for (int h = 0; h < 4; ++h) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + h * 32, r);
+            tc_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+                P4[((h * 32 + c) >> 2) * BM + rl] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                                                __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+        }
+    }
+    cluster_sync_all();   // every segment's partial tile visible cluster-wide
+    {
+        const int rl = (warp & 3) * 32 + lane, wg = warp >> 2;
+        const ExpTab tab = exp_tab_lane();
+        const uint32_t pbase = smem_u32(smem);
+        const int nq = (ncols + 3) >> 2;
+        const QkvRow qr = qkv_row(p, m0 + rl);
+        switch (S) {
+            case 1: combine_quads<1, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 2: combine_quads<2, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 3: combine_quads<3, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 4: combine_quads<4, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 5: combine_quads<5, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 6: combine_quads<6, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            case 7: combine_quads<7, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+            default: combine_quads<8, 1>(p, pbase, seg, wg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab, 2, v); break;
+        }
+    }
+    cluster_sync_all();   // peers keep their shared memory until every reader is done
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair(tbase, 2 * SUB_N);
+    }
+}
+
+cudaError_t launch_pair(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p, cudaStream_t stream,
+                        bool pdl) {
+    static std::atomic<uint64_t> attr_devs{0};
+    int dev = 0;
+    if (attrs_needed(attr_devs, &dev)) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        attrs_done(attr_devs, dev);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * p.ksplit, (p.ncols + 2 * SUB_N - 1) / (2 * SUB_N), p.n_out / (2 * BM));
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = kPairSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2 * p.ksplit;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, gemm_pair_kernel, tmW, tmX, p);
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -867,6 +1066,8 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
     // > 128 columns: 128-column tiles at two CTAs per SM (one CTA's epilogue overlaps the other's
     // main loop) beat 256-column tiles at one CTA per SM by 25 % on the 512-token prefill
+    if (p.pair > 0 && p.n_out % (2 * BM) == 0 && 2 * p.ksplit <= 16 && p.norm_x == nullptr && p.ss_out == nullptr)
+        return launch_pair(tmW, tmX, p, stream, pdl);
     if (p.max_nsub != 4) return launch_nsub<2>(tmW, tmX, p, stream, pdl);
     return launch_nsub<4>(tmW, tmX, p, stream, pdl);
 }

@@ -110,3 +110,23 @@ def test_wide_mma_form_is_bit_identical():
         check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y2.data_ptr(), n_out, K, ncols, n_out, -1, None))
         torch.cuda.synchronize()
         assert torch.equal(Y1.view(torch.int32), Y2.view(torch.int32))
+
+
+def test_cta_pair_gemm_bit_identical():
+    """The CTA-pair form (gemm_pair_kernel: tcgen05.mma.cta_group::2, M = 256, each CTA holding its
+    128 weight rows and half of the 128 activation columns) against the one-CTA form, S = 1..8 (up
+    to 16-CTA clusters): every output bit equal."""
+    import torch
+    from paper_2602_00182_b200._lib import lib, check
+
+    g = torch.Generator().manual_seed(5)
+    for n_out, K, ncols, S in [(256, 256, 65, 1), (256, 512, 128, 2), (512, 1024, 200, 2), (512, 4096, 256, 4),
+                               (768, 2048, 300, 5), (256, 4096, 129, 8), (1024, 1024, 512, 3)]:
+        W = _rand_bf16((n_out, K), g, 0.05)
+        X = _rand_bf16((ncols, K), g)
+        Y1 = torch.full((ncols, n_out), float("nan"), device="cuda")
+        Y2 = Y1.clone()
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y1.data_ptr(), n_out, K, ncols, n_out, S, None))
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y2.data_ptr(), n_out, K, ncols, n_out, 200 + S, None))
+        torch.cuda.synchronize()
+        assert torch.equal(Y1.view(torch.int32), Y2.view(torch.int32)), (n_out, K, ncols, S)
