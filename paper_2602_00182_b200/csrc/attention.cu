@@ -223,7 +223,6 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
                              m);
         }
     } tr{a, {a.trace != nullptr ? globaltimer_ns() : 0}};
-    const ExpTab tab = exp_tab_lane();   // issued before the dependency wait: off the critical path
     if (threadIdx.x == 0)
         l2_prefetch_slice(a.l2pf, a.l2pf_bytes, c + gridDim.x * (kvh + gridDim.y * col),
                           gridDim.x * gridDim.y * gridDim.z);
@@ -278,18 +277,29 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     auto load_rows = [&](int r_begin, int r_end) {
         load_chunk_rows<HD>(a, bt, kvh, p0, r_begin, r_end, sK, sV, true, true, tid);
     };
+    ExpTab tab;
     if (a.decode) {
         load_rows(0, pos - p0 < n ? pos - p0 : n);   // history rows, before the wait
+        tab = exp_tab_lane();                        // also before the wait, after the history loads
         pdl_wait();
         pdl_trigger();
         tr.mark(1);
         if (pos - p0 < n) load_rows(pos - p0, n);     // the row the QKV GEMM just appended
     } else {
+        tab = exp_tab_lane();
         load_rows(0, n);
     }
     cp_async_commit();
+    // q: 8 bf16 per 16-byte load (one L2 round trip), stored as f32 quads in qk_block8 order
     const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
-    for (int i = tid; i < G * HD; i += kNT) sQ[qperm(i)] = bf2f(qsrc[i]);   // quads in qk_block8 order
+    for (int i = tid * 8; i < G * HD; i += kNT * 8) {
+        const uint4 w = *reinterpret_cast<const uint4*>(qsrc + i);
+        *reinterpret_cast<float4*>(sQ + i) = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.y << 16),
+                                                         __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y & 0xffff0000u));
+        *reinterpret_cast<float4*>(sQ + i + 4) = make_float4(__uint_as_float(w.z << 16), __uint_as_float(w.w << 16),
+                                                             __uint_as_float(w.z & 0xffff0000u),
+                                                             __uint_as_float(w.w & 0xffff0000u));
+    }
     cp_async_wait_all();
     __syncthreads();
     tr.mark(2);   // K/V chunk and q in shared memory
