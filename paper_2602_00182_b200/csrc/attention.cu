@@ -629,22 +629,24 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
         __syncthreads();
         q0 = q1;
     }
-    // per-column tickets: the CTA holding a column's last chunk partial combines that column
-    __threadfence();
+    // per-column tickets: the CTA holding a column's last chunk partial combines that column. The
+    // ticket thread's fence after the barrier releases the whole CTA's partials (cumulativity), and
+    // the combining CTA's ticket thread fences again before the barrier its readers pass.
     __syncthreads();
     if (tid < Q) {
         s_last[tid] = 0;
         if (s_n[tid] > 0) {
             const int nch = (s_pos[tid] + CH) / CH;
             int* t = a.tickets + static_cast<int64_t>(col0 + tid) * a.hkv + kvh;
+            __threadfence();
             if (atomicAdd(t, 1) == nch - 1) {
                 s_last[tid] = 1;
                 *t = 0;   // re-armed for the next launch
+                __threadfence();
             }
         }
     }
     __syncthreads();
-    __threadfence();
     for (int q = 0; q < Q; ++q) {
         if (!s_last[q]) continue;   // block-uniform
         const int nch = (s_pos[q] + CH) / CH;
