@@ -453,17 +453,17 @@ cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
     return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G, CL>, a, scale);
 }
 
-// Prefill: one CTA per (chunk, kv head, block of Q = 16/G consecutive query columns): the chunk's
+// Prefill: one CTA per (chunk, kv head, block of Q = ROWS/G consecutive query columns): the chunk's
 // K/V is loaded once for the block instead of once per query. Per (query, head) row the
 // arithmetic is chunk_scores / chunk_softmax / chunk_pv's: each thread evaluates four score trees
 // over one K row (the K vector unpacked once for the four), and the PV chains of a dimension share
 // each V element. Chunk partials go to the workspace; the CTA completing a query's chunk count
 // (ticket per column) combines it exactly as attn_chunk_kernel's ticket combine.
-template <int HD, int G>
+template <int HD, int G, int ROWS>
 __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a, float scale) {
     constexpr int CH = kAttnChunk;
-    constexpr int Q = G >= 16 ? 1 : 16 / G;          // query columns per CTA
-    constexpr int R = Q * G;                         // (query, head) rows, 16
+    constexpr int Q = G >= ROWS ? 1 : ROWS / G;      // query columns per CTA
+    constexpr int R = Q * G;                         // (query, head) rows: ROWS
     constexpr int NV = HD / 8;
     constexpr int DEPTH = (NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1) + 1;
     constexpr int SR = R * CH / kNT;                 // score rows per thread (4)
@@ -665,15 +665,15 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
     }
 }
 
-template <int HD, int G>
+template <int HD, int G, int ROWS>
 cudaError_t launch_prefill(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    constexpr int Q = G >= 16 ? 1 : 16 / G;
+    constexpr int Q = G >= ROWS ? 1 : ROWS / G;
     constexpr size_t dsm = 2 * static_cast<size_t>(kAttnChunk) * HD * 2 + static_cast<size_t>(Q * G) * HD * 4 +
                            static_cast<size_t>(Q * G) * kAttnChunk * 4;
     static std::atomic<uint64_t> attr_devs{0};
     int dev = 0;
     if (attrs_needed(attr_devs, &dev)) {
-        cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel<HD, G, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(dsm));
         if (e != cudaSuccess) return e;
         attrs_done(attr_devs, dev);
@@ -689,14 +689,17 @@ cudaError_t launch_prefill(const AttnParams& a, cudaStream_t stream, bool pdl) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(HD)));
-    return cudaLaunchKernelEx(&cfg, attn_prefill_kernel<HD, G>, a, scale);
+    return cudaLaunchKernelEx(&cfg, attn_prefill_kernel<HD, G, ROWS>, a, scale);
 }
 
 // Cluster combine when the chunks of a (column, kv head) fit one cluster and the pushed partials
 // fit the leader's K/V buffer; the workspace/ticket combine otherwise.
 template <int HD, int G>
 cudaError_t launch_hg(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    if (!a.decode && a.prefill_blocks) return launch_prefill<HD, G>(a, stream, pdl);
+    // (query, head) rows per CTA: 16 for prompts up to ~1k columns, 32 above (each K/V chunk shared by
+    // more rows; measured crossover); per-row arithmetic identical
+    if (!a.decode && a.prefill_blocks)
+        return a.ncols >= 1024 ? launch_prefill<HD, G, 32>(a, stream, pdl) : launch_prefill<HD, G, 16>(a, stream, pdl);
     // many columns: the workspace/ticket combine schedules better than 12-CTA clusters
     const bool cl = (a.cluster_max_cols <= 0 || a.ncols <= a.cluster_max_cols) && a.max_chunks <= kMaxClusterChunks &&
                     static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 <= 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
