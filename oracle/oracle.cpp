@@ -687,10 +687,13 @@ static float tc_dot_segmented(const uint16_t* w, const uint16_t* x, const Segs& 
 static int g_gemm_mode = 0;   // 0: b200 (tcgen05) profile ; 1: reference canonical tree
 // y[r] = W[r,:] . x under the active accumulation profile. Profile 1 is det_matvec canonical_tree
 // (detcore.cpp:180-181): products of two bf16 values are exact in f32, then the reference tree.
-static void gemv(const uint16_t* W, int rows, int cols, const uint16_t* x, float* y) {
+// `rule_rows`: the row count of the engine GEMM this product is part of (the engine fuses
+// [wq; wk; wv] into one GEMM and interleaves gate/up into another, so the K-segment rule sees the
+// fused shape, engine.cu forward()); 0: rows.
+static void gemv(const uint16_t* W, int rows, int cols, const uint16_t* x, float* y, int rule_rows = 0) {
     if (g_gemm_mode == 0) {
         std::vector<Segs> segs((rows + 127) / 128);
-        for (int t = 0; t < int(segs.size()); ++t) segs[t] = tile_segments(rows, cols, t);
+        for (int t = 0; t < int(segs.size()); ++t) segs[t] = tile_segments(rule_rows > 0 ? rule_rows : rows, cols, t);
         parallel_for(rows, [&](int64_t r) { y[r] = tc_dot_segmented(W + size_t(r) * cols, x, segs[r / 128]); });
         return;
     }
@@ -775,9 +778,9 @@ static void forward_token(Session& s, uint32_t token, bool want_logits, float* l
     for (int l = 0; l < c.L; ++l) {
         const auto& Ly = m.layers[l];
         rmsnorm(x.data(), Ly.attn_norm.data(), d, c.eps, h.data());
-        gemv(Ly.wq.data(), qd, d, h.data(), q.data());
-        gemv(Ly.wk.data(), kd, d, h.data(), k.data());
-        gemv(Ly.wv.data(), kd, d, h.data(), v.data());
+        gemv(Ly.wq.data(), qd, d, h.data(), q.data(), qd + 2 * kd);   // the engine's fused QKV GEMM
+        gemv(Ly.wk.data(), kd, d, h.data(), k.data(), qd + 2 * kd);
+        gemv(Ly.wv.data(), kd, d, h.data(), v.data(), qd + 2 * kd);
         for (int vec = 0; vec < 2; ++vec) {
             float* arr = vec == 0 ? q.data() : k.data();
             const int nh = vec == 0 ? c.hq : c.hkv;
@@ -810,8 +813,8 @@ static void forward_token(Session& s, uint32_t token, bool want_logits, float* l
         gemv(Ly.wo.data(), d, qd, attn.data(), o.data());
         for (int i = 0; i < d; ++i) x[i] = x[i] + o[i];
         rmsnorm(x.data(), Ly.ffn_norm.data(), d, c.eps, h.data());
-        gemv(Ly.wg.data(), F, d, h.data(), g.data());
-        gemv(Ly.wu.data(), F, d, h.data(), u.data());
+        gemv(Ly.wg.data(), F, d, h.data(), g.data(), 2 * F);   // the engine's interleaved gate/up GEMM
+        gemv(Ly.wu.data(), F, d, h.data(), u.data(), 2 * F);
         for (int i = 0; i < F; ++i) {
             const float e = det_expf(-g[i]);
             const float sg = g[i] / (1.0f + e);
