@@ -282,24 +282,27 @@ def test_streamed_attention_global_ticket_keys():
 
 
 def test_llama8b_matches_oracle_golden():
-    """The 8B-shape path (BASELINE cfg 2's model) against the CPU oracle: tokens and out_hash of a
-    12-token prompt, greedy and nucleus decodes, equal the oracle's committed output
-    (tests/golden/llama8b_oracle.json, made by tests/golden/make_llama8b_golden.py)."""
+    """The 8B-shape path (BASELINE cfg 2's model) against the CPU oracle: tokens, logit bits and
+    out_hash of a 12-token prompt (greedy and nucleus) and a 70-token prompt (two attention chunks)
+    equal the oracle's committed output (tests/golden/llama8b_oracle.json, made by
+    tests/golden/make_llama8b_golden.py), at batch 1 and with all three requests batched."""
     import json
     from pathlib import Path
 
     from paper_2602_00182_b200.detcore import DecodePolicy, Engine
 
     g = json.loads((Path(__file__).parent / "golden" / "llama8b_oracle.json").read_text())
-    eng = Engine(g["model"], "b200", max_batch=2, max_context=64)
-    prompt = np.array(g["prompt"], dtype=np.uint32)
+    cases = g["cases"]
+    eng = Engine(g["model"], "b200", max_batch=len(cases), max_context=128)
+    prompts = [np.array(c["prompt"], dtype=np.uint32) for c in cases]
     pols = [DecodePolicy.greedy(c["max_tokens"]) if c["kind"] == 0 else DecodePolicy.nucleus(c["p"], c["max_tokens"])
-            for c in g["cases"]]
-    seeds = [c["seed"] for c in g["cases"]]
-    for bs in (1, 2):
-        toks, logits, hashes = eng.generate([prompt] * len(pols), pols, seeds, batch_size=bs)
-        for i, c in enumerate(g["cases"]):
+            for c in cases]
+    seeds = [c["seed"] for c in cases]
+    for bs in (1, len(cases)):
+        toks, logits, hashes = eng.generate(prompts, pols, seeds, batch_size=bs)
+        for i, c in enumerate(cases):
             assert toks[i].tolist() == c["tokens"], (bs, i)
             assert [int(x) for x in logits[i][0, :8].view(np.uint32)] == c["logit_bits_step0_first8"], (bs, i)
+            assert [int(x) for x in logits[i][-1, -8:].view(np.uint32)] == c["logit_bits_last_step_last8"], (bs, i)
             assert hashes[i].hex() == c["out_hash"], (bs, i)
     eng.close()
