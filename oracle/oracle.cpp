@@ -455,6 +455,7 @@ struct Config {
 static const Config kConfigs[] = {
     {"llama-tiny", 2, 256, 4, 2, 64, 768, 4096, 500000.0, 1e-5f},
     {"llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 500000.0, 1e-5f},
+    {"llama-mid", 2, 1024, 8, 2, 128, 3584, 32000, 500000.0, 1e-5f},   // 8B kernel shapes (hd 128, G 4), oracle-fast
 };
 static const Config* find_config(const char* model_id) {
     for (const auto& c : kConfigs) {

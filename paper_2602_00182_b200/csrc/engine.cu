@@ -1098,7 +1098,7 @@ int detgpu_create(int device, const char* model_id, const char* arch, uint32_t m
             const ModelConfig* c = find_model_config(model_id);
             if (c == nullptr)
                 return fail(nullptr, DETGPU_EINVAL,
-                            std::string("unknown model config for '") + model_id + "' (expected llama-tiny[:tag] or llama3-8b[:tag])");
+                            std::string("unknown model config for '") + model_id + "' (expected llama-tiny[:tag], llama-mid[:tag] or llama3-8b[:tag])");
             E->cfg = *c;
             if (int rc = init_weights(E)) return rc;
             if (int rc = init_buffers(E)) return rc;

@@ -19,6 +19,7 @@ inline const ModelConfig* find_model_config(const char* model_id) {
     static const ModelConfig kConfigs[] = {
         {"llama-tiny", 2, 256, 4, 2, 64, 768, 4096, 500000.0, 1e-5f},
         {"llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 500000.0, 1e-5f},
+        {"llama-mid", 2, 1024, 8, 2, 128, 3584, 32000, 500000.0, 1e-5f},   // 8B kernel shapes (hd 128, G 4), oracle-fast
     };
     for (const auto& c : kConfigs) {
         const size_t n = std::strlen(c.name);

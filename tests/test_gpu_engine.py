@@ -306,3 +306,29 @@ def test_llama8b_matches_oracle_golden():
             assert [int(x) for x in logits[i][-1, -8:].view(np.uint32)] == c["logit_bits_last_step_last8"], (bs, i)
             assert hashes[i].hex() == c["out_hash"], (bs, i)
     eng.close()
+
+
+def test_mid_model_bit_exact_with_oracle():
+    """llama-mid: the 8B kernel instantiations (head dim 128, 4 query heads per kv head, K-segment
+    rules of several shapes) at a size the oracle runs in seconds. 300- and 1,100-token prompts
+    (5 and 18 attention chunks: the cluster limit is 16, so decode takes the workspace combine),
+    greedy and nucleus, through the cluster/workspace and the streamed attention: tokens, f32
+    logits and out_hash equal the oracle's."""
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    O.lib().orc_set_threads(16)
+    om = O.Llama("llama-mid:t")
+    eng = Engine("llama-mid:t", "b200", max_batch=3, max_context=1200)
+    prompts = [_prompt(61, 300, eng.vocab), _prompt(62, 300, eng.vocab), _prompt(63, 1100, eng.vocab)]
+    specs = [(0, None, 6), (2, 0.9, 6), (0, None, 3)]
+    pols = [DecodePolicy.greedy(T) if k == 0 else DecodePolicy.nucleus(p, T) for k, p, T in specs]
+    seeds = [11, 12, 13]
+    ref = [om.generate(pr, kind=k, p=p, max_tokens=T, seed=sd) for pr, (k, p, T), sd in zip(prompts, specs, seeds)]
+    for min_cols, bs in ((0, 1), (0, 3), (1, 3)):
+        eng.set_option("attn_stream_min_cols", min_cols)
+        toks, logits, hashes = eng.generate(prompts, pols, seeds, batch_size=bs)
+        for i, (ot, ol) in enumerate(ref):
+            assert toks[i].tolist() == ot.tolist(), (min_cols, bs, i)
+            assert (logits[i].view(np.uint32) == ol.view(np.uint32)).all(), (min_cols, bs, i)
+            assert hashes[i] == O.out_hash(ot, ol), (min_cols, bs, i)
+    eng.close()
