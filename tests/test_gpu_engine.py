@@ -285,7 +285,8 @@ def test_llama8b_matches_oracle_golden():
     """The 8B-shape path (BASELINE cfg 2's model) against the CPU oracle: tokens, logit bits and
     out_hash of a 12-token prompt (greedy and nucleus) and a 70-token prompt (two attention chunks)
     equal the oracle's committed output (tests/golden/llama8b_oracle.json, made by
-    tests/golden/make_llama8b_golden.py), at batch 1 and with all three requests batched."""
+    tests/golden/make_llama8b_golden.py), at batch 1, with all three requests batched, and through
+    continuous batching on two slots."""
     import json
     from pathlib import Path
 
@@ -298,8 +299,8 @@ def test_llama8b_matches_oracle_golden():
     pols = [DecodePolicy.greedy(c["max_tokens"]) if c["kind"] == 0 else DecodePolicy.nucleus(c["p"], c["max_tokens"])
             for c in cases]
     seeds = [c["seed"] for c in cases]
-    for bs in (1, len(cases)):
-        toks, logits, hashes = eng.generate(prompts, pols, seeds, batch_size=bs)
+    for bs, cont in ((1, False), (len(cases), False), (2, True)):
+        toks, logits, hashes = eng.generate(prompts, pols, seeds, batch_size=bs, continuous=cont)
         for i, c in enumerate(cases):
             assert toks[i].tolist() == c["tokens"], (bs, i)
             assert [int(x) for x in logits[i][0, :8].view(np.uint32)] == c["logit_bits_step0_first8"], (bs, i)
