@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
     ap.add_argument("--sweep", default="auto", choices=["auto", "off"],
                     help="N=1: decode-step tok/s and step roofline at batch 1/8/64/256 (context 640)")
+    ap.add_argument("--traffic", default="auto", choices=["auto", "off"],
+                    help="N=1: DRAM bytes of one gate/up launch, measured by ncu in a subprocess")
     ap.add_argument("--cpu-sample-prompt", type=int, default=4)
     ap.add_argument("--cpu-sample-gen", type=int, default=2)
     return ap.parse_args()
@@ -162,9 +164,72 @@ def cpu_oracle_sample(model: str, prompt_len: int, gen: int, vocab_hint: int = 1
     dt = time.perf_counter() - t1
     del m
     return {"value": gen / dt, "unit": "tok/s", "cores": threads, "kind": "port",
-            "sample": f"{model}, 1 request, prompt {prompt_len} + {gen} generated tokens "
-                      f"({prompt_len + gen - 1} forward passes, {dt:.1f} s; weight generation {t_init:.1f} s excluded)",
-            "seconds": dt}
+            "sample": f"{model}: 1 request, prompt {prompt_len} tokens (one multi-column prefill) + {gen} generated "
+                      f"tokens, {dt:.1f} s; weight generation {t_init:.1f} s excluded. NOT the GPU arm's prompt "
+                      f"512 / gen 256: that request takes the oracle ~25-50 min on 8 cores "
+                      f"(tests/golden/make_llama8b_bench_golden.py)",
+            "same_config": False, "seconds": dt}
+
+
+GOLDEN = ROOT / "tests" / "golden" / "llama8b_bench_oracle.json"
+
+
+def measure_traffic(args, timeout_s: int = 240):
+    """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum of ONE gate/up GEMM launch
+    (layer 1 of an un-graphed decode step of this model at batch B, context prompt + gen/2;
+    tools/profile_step.py), counted by ncu in a subprocess during this bench run. Byte counts
+    only: no time measured under the profiler is reported."""
+    import shutil
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return None, "ncu not found"
+    # GEMM launches per layer: qkv, o, gate/up, down -> the 7th gemm_tc launch is layer 1's gate/up
+    cmd = [ncu, "--kernel-name", "regex:gemm_tc_kernel", "--launch-skip", "6", "--launch-count", "1",
+           "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--csv", "--clock-control", "none",
+           sys.executable, str(ROOT / "tools" / "profile_step.py"), "--model", args.model, "--batch", str(args.batch),
+           "--ctx", str(args.prompt + args.gen // 2)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except (subprocess.TimeoutExpired, OSError) as e:
+        return None, f"ncu failed: {str(e)[:120]}"
+    vals = {}
+    for ln in r.stdout.splitlines():
+        parts = [x.strip('"') for x in ln.split('","')]
+        if len(parts) >= 3 and parts[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            unit, v = parts[-2], float(parts[-1].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+            vals[parts[-3]] = v * scale
+    if len(vals) != 2:
+        return None, f"ncu rc={r.returncode}: metrics not found ({(r.stderr or r.stdout)[-160:]!r})"
+    return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"], \
+        "ncu (this run, subprocess): gate/up GEMM, layer 1, tools/profile_step.py; read {:.1f} MB + write {:.1f} MB".format(
+            vals["dram__bytes_read.sum"] / 1e6, vals["dram__bytes_write.sum"] / 1e6)
+
+
+def oracle_probes(args, eng, own: dict, rank: int):
+    """Compare this run's receipts with the CPU oracle's golden for the same workload. Greedy:
+    request 0's hash from the timed workload's e2e leg (rank 0). Nucleus: request 1 re-run with
+    p = 0.9 on every rank (all ranks must agree with the oracle)."""
+    from paper_2602_00182_b200 import replicas
+    from paper_2602_00182_b200.detcore import DecodePolicy
+
+    if not GOLDEN.exists():
+        return {"unavailable": "no golden file"}
+    g = json.loads(GOLDEN.read_text())
+    cases = {c["name"]: c for c in g["cases"]}
+    if g["model"] != args.model or any(c["prompt_len"] != args.prompt or c["max_tokens"] != args.gen
+                                       for c in cases.values()):
+        return {"unavailable": f"golden is for {g['model']} prompt 512 / gen 256"}
+    out = {}
+    if "greedy" in cases and 0 in own:
+        out["greedy_request0"] = own[0].hex() == cases["greedy"]["out_hash"]
+    if "nucleus" in cases:
+        c = cases["nucleus"]
+        _, _, h = eng.generate([replicas.synthetic_prompt(1, args.prompt, eng.vocab)], [DecodePolicy.nucleus(c["p"], args.gen)],
+                               [c["seed"]], batch_size=1, want_logits=False)
+        out["nucleus_request1"] = h[0].hex() == c["out_hash"]
+    return out
 
 
 def run_reference(args, rank: int, world: int):
@@ -193,8 +258,10 @@ def run_reference(args, rank: int, world: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * meta["seconds"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic prompts, random-init weights (counter-based from model_id)",
-            "config": {"workload": "llama3-8b shape greedy decode (bounded CPU sample)", "global_batch": 1,
-                       "seq_len": args.cpu_sample_prompt + args.cpu_sample_gen, "parallelism": "cpu threads"},
+            "config": {"workload": f"llama3-8b shape greedy decode, bounded CPU sample: prompt {args.cpu_sample_prompt}"
+                                   f" / gen {args.cpu_sample_gen} (GPU arm: prompt 512 / gen 256)", "global_batch": 1,
+                       "seq_len": args.cpu_sample_prompt + args.cpu_sample_gen, "parallelism": "cpu threads",
+                       "same_config": False},
             "cpu_baseline": {k: meta[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_toy_engine": ref_toy}
@@ -282,10 +349,18 @@ def run_ours(args, rank: int, world: int, local: int):
         v2_hash_ms += eng.last_stats.hash_ms
     v2_max = replicas.max_over_ranks(v2_s, local)
     e2e_v2 = replicas.sum_over_ranks(args.gen * args.batch * args.e2e_steps, local) / v2_max
-    # cross-GPU receipt equality: every rank runs the same probe request (global index 0)
-    _, _, probe = eng.generate([replicas.synthetic_prompt(0, args.prompt, V)], [DecodePolicy.greedy(args.gen)],
-                               [replicas.request_seed(0)], want_logits=False)
-    cross_equal = replicas.receipts_equal_across_ranks(probe, local)
+    # cross-GPU receipt equality by re-execution: every rank re-runs the requests that rank
+    # (rank + 1) mod N served above and the hashes are all-gathered (at N = 1 the "other" rank is
+    # this one: a replay). Request identity never depends on the rank (replicas.request_seed).
+    own = {g: hashes[0][i] for i, g in enumerate(gidx)}
+    nxt = (rank + 1) % world
+    gnext = [nxt * args.batch + i for i in range(args.batch)]
+    _, _, hn = eng.generate([replicas.synthetic_prompt(g, args.prompt, V) for g in gnext], pols,
+                            [replicas.request_seed(g) for g in gnext], batch_size=args.batch, want_logits=False)
+    cross = replicas.cross_rank_reexecution(own, dict(zip(gnext, hn)), local)
+    # the CPU oracle's output for this exact workload (tests/golden/llama8b_bench_oracle.json):
+    # request 0 (greedy, this bench's own request) and request 1 (nucleus p = 0.9)
+    oracle_probe = oracle_probes(args, eng, own, rank)
 
     # ---- roofline: live per-kernel timing of one un-graphed decode step (CUDA events per launch)
     import ctypes as C
@@ -304,13 +379,27 @@ def run_ours(args, rank: int, world: int, local: int):
     sb = step_bytes(info, B, args.prompt, args.gen)
     step_ms_profiled = sum(cls_ms.values())
     step_ms_graph = decode_ms / max(1, args.steps * (args.gen - 1))
+    # the same kernel INSIDE the CUDA-graph step (PDL pipeline): per-CTA timeline, first dependency
+    # release -> last CTA end of each gate/up launch (paper_2602_00182_b200/timeline.py)
+    graph_span = None
+    try:
+        from paper_2602_00182_b200 import timeline
+
+        spans, g_ms, g_us = timeline.graph_step_spans(eng, args.batch, args.prompt + args.gen // 2)
+        gu = spans.get("gate_up_gemm", [])
+        graph_span = {"gate_up_us_mean": float(np.mean(gu)) if gu else None, "launches": len(gu),
+                      "achieved_GBs": gu_bytes / (float(np.mean(gu)) * 1e-6) / 1e9 if gu else None,
+                      "traced_step_us": g_us, "graph_ms_per_step": g_ms,
+                      "class_share_of_step": {k: round(float(np.sum(v)) / g_us, 4) for k, v in spans.items()}}
+    except Exception as e:   # noqa: BLE001
+        graph_span = {"unavailable": str(e)[:200]}
     traffic = None
-    tf = ROOT / "profiles" / "gate_up_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    traffic_src = None
 
     if rank != 0:
         return
+    if args.traffic == "auto" and world == 1:
+        traffic, traffic_src = measure_traffic(args)
     sweep = None
     if args.sweep == "auto" and world == 1:
         try:
@@ -345,6 +434,7 @@ def run_ours(args, rank: int, world: int, local: int):
                                    "GPU (DESIGN.md §3.9); tokens + 32 B/step D2H"},
         "roofline": {"bound": "hbm", "kernel": "gate_up_gemm (tcgen05, SwiGLU epilogue)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src, "in_graph": graph_span,
                      "peak_source": peak_kind, "bytes_per_launch": gu_bytes, "launch_ms": gu_launch_ms,
                      "step": {"algorithmic_bytes": sb, "graph_step_ms": step_ms_graph,
                               "achieved_GBs": sb / (step_ms_graph / 1000.0) / 1e9 if step_ms_graph else None,
@@ -354,8 +444,11 @@ def run_ours(args, rank: int, world: int, local: int):
         "clocks": clk.summary(),
         "gpu_launches": int(launches_all),
         "decode_tok_s": decode_tok_s, "prefill_ms": prefill_ms / args.steps,
-        "replay_match_rate": replay_rate, "cross_gpu_receipts_equal": bool(cross_equal),
-        "receipt_probe_out_hash": probe[0].hex(),
+        "replay_match_rate": replay_rate, "cross_gpu_receipts_equal": bool(cross["all_equal"]),
+        "cross_gpu_reexecution": cross,
+        "receipt_probe_out_hash": hashes[0][0].hex(),
+        "receipt_probe_matches_oracle": oracle_probe.get("greedy_request0"),
+        "oracle_probes": oracle_probe,
         "decode_batch_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
@@ -365,7 +458,13 @@ def main():
     args = parse()
     from paper_2602_00182_b200 import replicas
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without torchrun: launch the N ranks ourselves (one process per
+        # GPU, the same torchrun command the driver uses) and pass rank 0's JSON line through.
+        sys.exit(replicas.launch_local(args.gpus, [str(Path(__file__).resolve())] + sys.argv[1:]))
     rank, world, local = replicas.dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         if world > 1:
             replicas.init("gloo")

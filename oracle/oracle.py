@@ -29,6 +29,7 @@ def lib():
         sig = {
             "orc_set_threads": (None, [i32]), "orc_get_threads": (i32, []),
             "orc_set_gemm_mode": (None, [i32]), "orc_tc_dot": (f32, [vp, vp, i32]),
+            "orc_tc_dot_fast": (f32, [vp, vp, i32]), "orc_have_avx2": (i32, []),
             "orc_gemm": (None, [vp, vp, i32, i32, i32, vp]),
             "orc_fnv1a64": (u64, [C.c_char_p]), "orc_mix_seed": (u64, [u64, u64]),
             "orc_prng_seeded": (None, [u64, vp]), "orc_prng_next_u64": (u64, [vp]),

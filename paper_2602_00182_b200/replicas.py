@@ -92,3 +92,46 @@ def receipts_equal_across_ranks(hashes: Sequence[bytes], device=None) -> bool:
     parts = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, mine)
     return all(torch.equal(p, parts[0]) for p in parts)
+
+
+def launch_local(n: int, argv: Sequence[str], master_port: int = 0) -> int:
+    """Run `python argv...` as n local ranks (one per GPU) exactly as the driver does for N > 1:
+    ``python -m torch.distributed.run --nnodes=1 --nproc-per-node n --master-addr 127.0.0.1``.
+    Children inherit stdout, so rank 0's output is this process's output. Returns the exit code."""
+    import socket
+    import subprocess
+    import sys
+
+    if master_port == 0:
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        master_port = s.getsockname()[1]
+        s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(master_port), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def cross_rank_reexecution(own: dict, rerun: dict, device=None) -> dict:
+    """Cross-GPU receipt equality by re-execution: every rank passes
+    the out_hashes of the requests it served ({global index: hash}) and of the requests of
+    ANOTHER rank that it re-executed. All-gathered; every re-executed request's hash must equal
+    the serving rank's. Returns {"requests", "reexecuted", "all_equal", "mismatches"}."""
+    import torch.distributed as dist
+
+    mine = ({int(k): bytes(v) for k, v in own.items()}, {int(k): bytes(v) for k, v in rerun.items()})
+    if dist.is_available() and dist.is_initialized():
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, mine)
+    else:
+        parts = [mine]
+    served, again = {}, {}
+    for o, r in parts:
+        served.update(o)
+        for k, v in r.items():
+            again.setdefault(k, []).append(v)
+    bad = sorted(k for k, vs in again.items() if k not in served or any(v != served[k] for v in vs))
+    return {"requests": len(served), "reexecuted": sum(len(v) for v in again.values()), "all_equal": not bad,
+            "mismatches": bad[:16]}
