@@ -93,7 +93,8 @@ int detgpu_arch_supported(const char* arch);
  *   arch "archA" / "archB": the reference ToyModel with that accumulation profile, any model_id
  *                           (weights from fnv1a64(model_id), detcore.cpp:275-296);
  *   arch "b200": a Llama-style transformer whose shape is named by the model_id prefix
- *                ("llama-tiny" | "llama3-8b"), weights counter-generated from fnv1a64(model_id).
+ *                ("llama-tiny" | "llama-mid" | "llama3-8b", optionally ":tag"), weights
+ *                counter-generated from fnv1a64(model_id).
  * max_batch: requests decoded together (1..256); max_context: prompt + generated tokens.
  * Replaces ToyModel::from_model_id + ArchRegistry::find (detcore.cpp:288, 333).
  */
@@ -108,6 +109,9 @@ const char* detgpu_last_error(const detgpu_engine* h);
  * Requests are decoded in groups of at most batch_size (0 -> DETGPU_EINVAL, detcore.cpp:389);
  * the bytes of each request do not depend on the grouping.
  *   prompts[i][0..prompt_lens[i]) token ids; seeds[i] seeds the request's xoshiro256++ stream.
+ *                    An empty prompt is accepted as the reference accepts it (detcore.cpp:340-352):
+ *                    for "b200" it means the one-token prompt [0] (BOS), for the ToyModel the
+ *                    zero state.
  *   tokens_out[i]  : policies[i].max_tokens u32 (may be NULL with DETGPU_F_DEVICE_ONLY)
  *   logits_out     : NULL, or an array of n_req pointers each NULL or max_tokens*vocab f32
  *   out_hash       : NULL or n_req*32 bytes: SHA-256 of the canonical output bytes
@@ -219,9 +223,12 @@ int detgpu_k_init_tensor(void* dst, uint64_t seed, int64_t rows, int64_t cols, i
  * is advanced once per row. tokens_out [rows]. Policies host array of `rows`. */
 int detgpu_k_sample(const float* logits, int rows, int vocab, const detgpu_policy* policies, uint64_t* prng_state,
                     uint32_t* tokens_out, float* probs_out, int32_t* status_out, void* stream);
-/* Decode attention for `ncols` queries against a contiguous (non-paged) cache:
- *   q [ncols][hq*hd] bf16, k/v [ncols? no: per query col] -> see tests/test_gpu_kernels.py. */
+/* Receipt v2 roots of n_steps rows of `vocab` f32 logits: roots [n_steps][32]. */
 int detgpu_k_step_roots(const float* trace, int n_steps, int vocab, uint8_t* roots, void* stream);
+/* Decode attention (the engine's cluster / streamed kernels) for `ncols` query columns over the
+ * PAGED cache: q [ncols][hq*hd] bf16; kcache / vcache [page][hkv][page positions][hd] bf16;
+ * block_table [req][max_pages] page ids; col_pos[c] = the column's position (it attends to
+ * [0, col_pos[c]]); col_req[c] its request row of block_table; out [ncols][hq*hd] bf16. */
 int detgpu_k_attention(const void* q, const void* kcache, const void* vcache, const int32_t* block_table,
                        const int32_t* col_pos, const int32_t* col_req, void* out, int ncols, int hq, int hkv,
                        int hd, int page, int max_pages, void* stream);

@@ -4,7 +4,9 @@
 // libdetgpu.so; see INTEGRATION.md. Requires C++17.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <climits>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -61,35 +63,148 @@ struct InferenceOutput {   // detcore.hpp:79-85, plus the receipt's out_hash
     Hash32 out_hash{};
 };
 
+// ---- approved profiles (detcore.hpp:21-45, detcore.cpp:12-26) ----
+// The reference's profiles name an accumulation order; the GPU engine runs canonical_tree and
+// sequential on the reference ToyModel (engine arch "archA" / "archB") and tcgen05_b200 on the
+// Llama-style transformer (engine arch "b200"). A caller's registry may add more names for these
+// orders, exactly as the reference's ArchRegistry::add does.
+enum class ReductionOrder : uint8_t { canonical_tree = 0, sequential = 1, tcgen05_b200 = 2 };
+enum class FmaEmulation : uint8_t { fused = 0, split = 1 };
+
+struct ArchProfile {
+    std::string name;
+    ReductionOrder reduction_order = ReductionOrder::canonical_tree;
+    FmaEmulation fma_emulation = FmaEmulation::split;
+};
+
+class ArchRegistry {
+public:
+    static const ArchRegistry& defaults() {
+        static const ArchRegistry reg = [] {
+            ArchRegistry r;
+            r.add({"archA", ReductionOrder::canonical_tree, FmaEmulation::fused});
+            r.add({"archB", ReductionOrder::sequential, FmaEmulation::split});
+            r.add({"b200", ReductionOrder::tcgen05_b200, FmaEmulation::fused});
+            return r;
+        }();
+        return reg;
+    }
+    void add(ArchProfile p) { profiles_[p.name] = std::move(p); }
+    const ArchProfile* find(const std::string& name) const {
+        auto it = profiles_.find(name);
+        return it == profiles_.end() ? nullptr : &it->second;
+    }
+    bool contains(const std::string& name) const { return find(name) != nullptr; }
+    std::vector<std::string> names() const {
+        std::vector<std::string> v;
+        for (auto& kv : profiles_) v.push_back(kv.first);
+        return v;
+    }
+
+private:
+    std::map<std::string, ArchProfile> profiles_;
+};
+
+// ---- engine cache ----
+// One engine per (device, model_id, engine arch) holds the weights resident. Sized from the
+// requests: an engine is rebuilt with a larger context when a request needs it (the reference
+// accepts any length). A per-engine mutex serialises generate + copy-out (the reference's infer
+// is pure and thread-safe; the handle is not). At most max_engines stay cached (least recently
+// used dropped); release_engines() frees them all (an engine still in use by another thread is
+// destroyed when that call returns).
+struct EngineOptions {
+    uint32_t max_batch = 64;       // decode slots per engine (larger batch_size runs in groups: same bytes)
+    uint32_t min_context = 2048;   // initial context capacity; grown to the next power of two on demand
+    size_t max_engines = 4;
+};
+
 namespace detail {
-// One engine per (device, model_id, arch): weights are generated once and stay resident.
-inline detgpu_engine* engine_for(const ExecutionTuple& e, int device) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, std::string, std::string>, detgpu_engine*> engines;
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(device, e.model_id, e.arch);
-    auto it = engines.find(key);
-    if (it != engines.end()) return it->second;
+struct CachedEngine {
     detgpu_engine* h = nullptr;
-    const int rc = detgpu_create(device, e.model_id.c_str(), e.arch.c_str(), 64, 2048, &h);
+    uint32_t max_context = 0;
+    uint64_t last_used = 0;
+    std::mutex mu;
+    ~CachedEngine() {
+        if (h) detgpu_destroy(h);
+    }
+};
+struct Cache {
+    std::mutex mu;
+    EngineOptions opt;
+    uint64_t clock = 0;
+    std::map<std::tuple<int, std::string, std::string>, std::shared_ptr<CachedEngine>> engines;
+};
+inline Cache& cache() {
+    static Cache c;
+    return c;
+}
+inline const char* engine_arch(const ArchProfile& p) {
+    switch (p.reduction_order) {
+        case ReductionOrder::canonical_tree: return "archA";
+        case ReductionOrder::sequential: return "archB";
+        default: return "b200";
+    }
+}
+inline std::shared_ptr<CachedEngine> engine_for(const std::string& model_id, const char* arch, uint32_t need_ctx,
+                                                int device) {
+    Cache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto key = std::make_tuple(device, model_id, std::string(arch));
+    auto it = c.engines.find(key);
+    if (it != c.engines.end() && it->second->max_context >= need_ctx) {
+        it->second->last_used = ++c.clock;
+        return it->second;
+    }
+    uint32_t ctx = std::max<uint32_t>(1, c.opt.min_context);
+    while (ctx < need_ctx) ctx *= 2;
+    if (it == c.engines.end() && c.engines.size() >= std::max<size_t>(1, c.opt.max_engines)) {
+        auto victim = c.engines.begin();
+        for (auto v = c.engines.begin(); v != c.engines.end(); ++v)
+            if (v->second->last_used < victim->second->last_used) victim = v;
+        c.engines.erase(victim);
+    }
+    auto e = std::make_shared<CachedEngine>();
+    const bool toy = std::string(arch) != "b200";
+    const int rc = detgpu_create(device, model_id.c_str(), arch, c.opt.max_batch, toy ? 1 : ctx, &e->h);
     if (rc == DETGPU_EINVAL) throw std::invalid_argument(detgpu_global_error());
     if (rc != DETGPU_OK) throw std::runtime_error(detgpu_global_error());
-    engines[key] = h;
-    return h;
+    e->max_context = toy ? UINT32_MAX : ctx;
+    e->last_used = ++c.clock;
+    c.engines[key] = e;
+    return e;
 }
 }  // namespace detail
 
-// detcore.cpp:387-410. Groups by (model_id, arch); per-tuple bytes equal individual infer().
+inline void set_engine_options(const EngineOptions& o) {
+    std::lock_guard<std::mutex> lk(detail::cache().mu);
+    detail::cache().opt = o;
+}
+inline void release_engines() {
+    std::lock_guard<std::mutex> lk(detail::cache().mu);
+    detail::cache().engines.clear();
+}
+
+// detcore.cpp:387-410. Groups by (model_id, profile); per-tuple bytes equal individual infer().
+// Validation before any work, in the reference's order (unknown arch, then policy, then tokens).
 inline std::vector<InferenceOutput> infer_batch(const std::vector<ExecutionTuple>& execs, size_t batch_size,
+                                                const ArchRegistry& registry = ArchRegistry::defaults(),
                                                 int device = 0) {
     if (batch_size == 0) throw std::invalid_argument("infer_batch: batch_size must be positive");
     std::vector<InferenceOutput> out(execs.size());
     std::map<std::pair<std::string, std::string>, std::vector<size_t>> groups;
-    for (size_t i = 0; i < execs.size(); ++i) groups[{execs[i].model_id, execs[i].arch}].push_back(i);
+    for (size_t i = 0; i < execs.size(); ++i) {
+        const ArchProfile* prof = registry.find(execs[i].arch);
+        if (prof == nullptr) throw std::invalid_argument("infer: unknown arch profile '" + execs[i].arch + "'");
+        groups[{execs[i].model_id, detail::engine_arch(*prof)}].push_back(i);
+    }
     for (auto& [key, idx] : groups) {
-        if (!detgpu_arch_supported(key.second.c_str()))
-            throw std::invalid_argument("infer: unknown arch profile '" + key.second + "'");
-        detgpu_engine* h = detail::engine_for(execs[idx[0]], device);
+        uint32_t need = 1;
+        for (size_t i : idx)
+            need = std::max<uint32_t>(need, static_cast<uint32_t>(std::max<size_t>(execs[i].prompt.size(), 1)) +
+                                                execs[i].decode_policy.max_tokens);
+        std::shared_ptr<detail::CachedEngine> eng = detail::engine_for(key.first, key.second.c_str(), need, device);
+        std::lock_guard<std::mutex> use(eng->mu);
+        detgpu_engine* h = eng->h;
         detgpu_model_info info{};
         detgpu_get_model_info(h, &info);
         const size_t n = idx.size();
@@ -135,7 +250,10 @@ inline std::vector<InferenceOutput> infer_batch(const std::vector<ExecutionTuple
 }
 
 // detcore.cpp:380-385
-inline InferenceOutput infer(const ExecutionTuple& e, int device = 0) { return infer_batch({e}, 1, device)[0]; }
+inline InferenceOutput infer(const ExecutionTuple& e, const ArchRegistry& registry = ArchRegistry::defaults(),
+                             int device = 0) {
+    return infer_batch({e}, 1, registry, device)[0];
+}
 
 // receipts.cpp:119 req_hash
 inline Hash32 req_hash(const ExecutionTuple& e) {

@@ -1257,7 +1257,14 @@ int orc_llama_generate(void* h, const uint32_t* prompt, uint32_t plen, int kind,
     pol.p = p;
     pol.max_tokens = max_tokens;
     if (!pol.valid()) return 1;
-    if (plen == 0) return 1;
+    // An empty prompt is the one-token prompt [0] (BOS; the engine's kBosToken rule).
+    // The reference's ToyModel accepts empty prompts (detcore.cpp:340-352); a transformer needs a
+    // position to predict from.
+    static const uint32_t kBos[1] = {0};
+    if (plen == 0) {
+        prompt = kBos;
+        plen = 1;
+    }
     for (uint32_t i = 0; i < plen; ++i)
         if (prompt[i] >= uint32_t(m->cfg.V)) return 1;
     if (max_tokens == 0) return 0;

@@ -109,6 +109,18 @@ struct Engine {
     size_t hash_next = 0;            // round-robin victim when every buffer is busy
     // decode graphs keyed by (ncols, slot_stride)
     std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
+    std::map<std::pair<int, int64_t>, uint64_t> graph_used;   // LRU stamps (get_graph)
+    uint64_t graph_clock = 0;
+    // pinned host staging for the serving loop's small H2D copies (admission state, prefill
+    // plans): ring of buffers, each reused only after the event recorded behind its copies
+    struct Stage {
+        void* p = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ev = nullptr;
+        bool pending = false;
+    };
+    Stage stage[4];
+    int stage_next = 0;
     uint64_t launches_per_step = 0;
     bool use_pdl = true;
     // toy model
@@ -160,6 +172,10 @@ struct Engine {
             if (p) cudaFreeHost(p);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
+        for (auto& st : stage) {
+            if (st.ev) cudaEventSynchronize(st.ev), cudaEventDestroy(st.ev);
+            if (st.p) cudaFreeHost(st.p);
+        }
         toy_free(toyw);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -171,6 +187,34 @@ int fail(Engine* e, int code, const std::string& msg) {
     if (e) e->err = msg;
     set_global_error(msg);
     return code;
+}
+
+constexpr size_t kMaxGraphs = 24;
+constexpr uint32_t kBosToken = 0;   // what an empty b200 prompt means (detgpu_generate)
+
+// Next pinned staging buffer of at least `bytes` (waits only if its previous copies are still
+// queued); stage_release() records the event behind the copies issued from it.
+cudaError_t stage_acquire(Engine* E, size_t bytes, void** out, int* idx) {
+    const int i = E->stage_next++ % 4;
+    Engine::Stage& st = E->stage[i];
+    cudaError_t e = cudaSuccess;
+    if (st.ev == nullptr && (e = cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if (st.pending && (e = cudaEventSynchronize(st.ev)) != cudaSuccess) return e;
+    st.pending = false;
+    if (st.cap < bytes) {
+        if (st.p) cudaFreeHost(st.p);
+        st.p = nullptr;
+        st.cap = 0;
+        if ((e = cudaHostAlloc(&st.p, bytes, cudaHostAllocDefault)) != cudaSuccess) return e;
+        st.cap = bytes;
+    }
+    *out = st.p;
+    *idx = i;
+    return cudaSuccess;
+}
+cudaError_t stage_release(Engine* E, int idx) {
+    E->stage[idx].pending = true;
+    return cudaEventRecord(E->stage[idx].ev, E->stream);
 }
 
 #define ENG_CUDA(expr)                                                                                 \
@@ -557,6 +601,10 @@ cudaError_t head_and_sample(Engine* E, const __nv_bfloat16* X, int ncols, uint64
 }
 
 int ensure_outputs(Engine* E, int nslots, int tmax) {
+    // the slot stride is bucketed (powers of two up to 64 steps, then multiples of 64) so a server
+    // seeing many distinct max_tokens captures a bounded set of decode graphs (layout only: the
+    // logits of step t of a slot are at slot * stride + t * V whatever the stride)
+    tmax = tmax <= 64 ? (tmax <= 1 ? 1 : 1 << (32 - __builtin_clz(unsigned(tmax - 1)))) : (tmax + 63) / 64 * 64;
     const size_t need_trace = size_t(nslots) * tmax * E->cfg.V;
     if (need_trace > E->trace_cap) {
         if (E->trace) cudaFree(E->trace);
@@ -565,6 +613,7 @@ int ensure_outputs(Engine* E, int nslots, int tmax) {
         E->trace_cap = need_trace;
         for (auto& gph : E->graphs) cudaGraphExecDestroy(gph.second);
         E->graphs.clear();
+        E->graph_used.clear();
     }
     const size_t need_tok = size_t(nslots) * tmax;
     if (need_tok > E->tok_cap) {
@@ -574,6 +623,7 @@ int ensure_outputs(Engine* E, int nslots, int tmax) {
         E->tok_cap = need_tok;
         for (auto& gph : E->graphs) cudaGraphExecDestroy(gph.second);
         E->graphs.clear();
+        E->graph_used.clear();
     }
     if (E->tcap != tmax || E->slot_stride != int64_t(tmax) * E->cfg.V) {
         E->tcap = tmax;
@@ -584,10 +634,20 @@ int ensure_outputs(Engine* E, int nslots, int tmax) {
 
 int get_graph(Engine* E, int ncols, cudaGraphExec_t* out) {
     auto key = std::make_pair(ncols, E->slot_stride);
+    E->graph_used[key] = ++E->graph_clock;
     auto it = E->graphs.find(key);
     if (it != E->graphs.end()) {
         *out = it->second;
         return DETGPU_OK;
+    }
+    if (E->graphs.size() >= kMaxGraphs) {   // bounded cache: drop the least recently used graph
+        auto victim = E->graphs.end();
+        for (auto g = E->graphs.begin(); g != E->graphs.end(); ++g)
+            if (victim == E->graphs.end() || E->graph_used[g->first] < E->graph_used[victim->first]) victim = g;
+        ENG_CUDA(cudaStreamSynchronize(E->stream));   // never destroy a graph that may still run
+        cudaGraphExecDestroy(victim->second);
+        E->graph_used.erase(victim->first);
+        E->graphs.erase(victim);
     }
     cudaGraph_t g;
     ENG_CUDA(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
@@ -917,7 +977,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
     uint64_t nl = 0, decode_steps = 0;
     Timer tall;
     double prefill_ms = 0;
-    std::vector<int> ctok, cpos, creq, lin, lout, adm, pstep, pslot;
+    std::vector<int> ctok, cpos, creq, lin, lout, adm;
     std::vector<std::future<void>> hashers;   // v1 receipts hashed off the decode loop
     struct Join {
         std::vector<std::future<void>>& h;
@@ -927,7 +987,19 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         }
     } join{hashers};
     for (;;) {
-        // admit pending requests into free slots (max_tokens == 0 needs no GPU work)
+        // 1. collect the slots that finished (the stream is idle here: synchronised at the end of
+        //    the previous round), freeing them for admission in this round
+        for (uint32_t sl = 0; sl < slots; ++sl) {
+            if (slot_req[sl] < 0 || slot_left[sl] != 0) continue;
+            const int r = slot_req[sl];
+            if (int rc = collect_slot(E, static_cast<int>(sl), pols[r].max_tokens, tokens_out ? tokens_out[r] : nullptr,
+                                      logits_out ? logits_out[r] : nullptr, out_hash ? out_hash + 32 * size_t(r) : nullptr,
+                                      v2, st, &hashers))
+                return rc;
+            slot_req[sl] = -1;
+        }
+        // 2. admit pending requests into free slots (max_tokens == 0 needs no GPU work). Nothing
+        //    below waits for the GPU: the small H2D copies come from pinned staging buffers.
         adm.clear();
         for (uint32_t sl = 0; sl < slots && next < n_req; ++sl) {
             if (slot_req[sl] >= 0) continue;
@@ -944,33 +1016,51 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         }
         if (!adm.empty()) {
             Timer tp;
-            for (int sl : adm) {   // the slot's decode state before its first token is sampled
-                const int r = slot_req[sl];
-                uint64_t pr[4];
-                prng_seeded(seeds[r], pr);
-                const DevPolicy dp = to_dev_policy(pols[r]);
-                const int pos = static_cast<int>(lens[r]) - 1, z = 0;
-                ENG_CUDA(cudaMemcpyAsync(E->d_prng + 4 * size_t(sl), pr, sizeof(pr), cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->d_pol + sl, &dp, sizeof(dp), cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->d_pos + sl, &pos, sizeof(int), cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->d_status + sl, &z, sizeof(int), cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaStreamSynchronize(s));   // the host values above live on this frame
-                if (st) st->h2d_bytes += sizeof(pr) + sizeof(dp) + 2 * sizeof(int);
+            struct AdmState {   // the slot's decode state before its first token is sampled
+                uint64_t prng[4];
+                DevPolicy dp;
+                int pos, status;
+            };
+            void* sp = nullptr;
+            int si = 0;
+            ENG_CUDA(stage_acquire(E, sizeof(AdmState) * adm.size(), &sp, &si));
+            AdmState* as = static_cast<AdmState*>(sp);
+            for (size_t j = 0; j < adm.size(); ++j) {
+                const int sl = adm[j], r = slot_req[sl];
+                prng_seeded(seeds[r], as[j].prng);
+                as[j].dp = to_dev_policy(pols[r]);
+                as[j].pos = static_cast<int>(lens[r]) - 1;
+                as[j].status = 0;
+                ENG_CUDA(cudaMemcpyAsync(E->d_prng + 4 * size_t(sl), as[j].prng, sizeof(as[j].prng), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_pol + sl, &as[j].dp, sizeof(DevPolicy), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_pos + sl, &as[j].pos, sizeof(int), cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->d_status + sl, &as[j].status, sizeof(int), cudaMemcpyHostToDevice, s));
+                if (st) st->h2d_bytes += sizeof(as[j].prng) + sizeof(DevPolicy) + 2 * sizeof(int);
             }
+            ENG_CUDA(stage_release(E, si));
             auto flush = [&]() -> int {
                 if (ctok.empty()) return DETGPU_OK;
                 const int nc = static_cast<int>(ctok.size());
-                ENG_CUDA(cudaMemcpyAsync(E->p_tok, ctok.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->p_pos, cpos.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->p_req, creq.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s));
                 const int nlast = static_cast<int>(lin.size());
+                void* bp = nullptr;
+                int bi = 0;
+                ENG_CUDA(stage_acquire(E, sizeof(int) * (3 * size_t(nc) + 2 * size_t(nlast)), &bp, &bi));
+                int* b = static_cast<int*>(bp);
+                std::copy(ctok.begin(), ctok.end(), b);
+                std::copy(cpos.begin(), cpos.end(), b + nc);
+                std::copy(creq.begin(), creq.end(), b + 2 * nc);
+                std::copy(lin.begin(), lin.end(), b + 3 * nc);
+                std::copy(lout.begin(), lout.end(), b + 3 * nc + nlast);
+                ENG_CUDA(cudaMemcpyAsync(E->p_tok, b, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->p_pos, b + nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                ENG_CUDA(cudaMemcpyAsync(E->p_req, b + 2 * nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
                 if (nlast > 0) {
-                    ENG_CUDA(cudaMemcpyAsync(E->p_last_in, lin.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
-                    ENG_CUDA(cudaMemcpyAsync(E->p_last_out, lout.data(), sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_in, b + 3 * nc, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_out, b + 3 * nc + nlast, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
                 }
+                ENG_CUDA(stage_release(E, bi));
                 if (st) st->h2d_bytes += sizeof(int) * (3ull * nc + 2ull * nlast) + sizeof(uint32_t) * nc;
                 ENG_CUDA(forward(E, nc, E->p_tok, E->p_pos, E->p_req, false, nlast, &nl));
-                ENG_CUDA(cudaStreamSynchronize(s));
                 ctok.clear();
                 cpos.clear();
                 creq.clear();
@@ -994,47 +1084,33 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
             }
             if (int rc = flush()) return rc;
             // first token of each admitted request: compact columns, trace step 0 of its slot
-            pstep.assign(adm.size(), 0);
-            pslot.assign(adm.begin(), adm.end());
-            ENG_CUDA(cudaMemcpyAsync(E->p_last_in, pstep.data(), sizeof(int) * pstep.size(), cudaMemcpyHostToDevice, s));
-            ENG_CUDA(cudaMemcpyAsync(E->p_last_out, pslot.data(), sizeof(int) * pslot.size(), cudaMemcpyHostToDevice, s));
+            void* pp = nullptr;
+            int pi = 0;
+            ENG_CUDA(stage_acquire(E, 2 * sizeof(int) * adm.size(), &pp, &pi));
+            int* pb = static_cast<int*>(pp);
+            for (size_t j = 0; j < adm.size(); ++j) {
+                pb[j] = 0;
+                pb[adm.size() + j] = adm[j];
+            }
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_in, pb, sizeof(int) * adm.size(), cudaMemcpyHostToDevice, s));
+            ENG_CUDA(cudaMemcpyAsync(E->p_last_out, pb + adm.size(), sizeof(int) * adm.size(), cudaMemcpyHostToDevice, s));
+            ENG_CUDA(stage_release(E, pi));
             ENG_CUDA(head_and_sample(E, E->h_last, static_cast<int>(adm.size()), &nl, false, E->p_last_in,
                                      E->p_last_out, true));
-            ENG_CUDA(cudaStreamSynchronize(s));
             for (int sl : adm) slot_left[sl] = static_cast<int>(pols[slot_req[sl]].max_tokens) - 1;
             prefill_ms += tp.ms();
         }
-        // collect finished slots, then run decode steps until the next one finishes
-        bool any = false;
-        for (uint32_t sl = 0; sl < slots; ++sl) {
-            if (slot_req[sl] < 0) continue;
-            if (slot_left[sl] == 0) {
-                const int r = slot_req[sl];
-                if (int rc = collect_slot(E, static_cast<int>(sl), pols[r].max_tokens, tokens_out ? tokens_out[r] : nullptr,
-                                          logits_out ? logits_out[r] : nullptr,
-                                          out_hash ? out_hash + 32 * size_t(r) : nullptr, v2, st, &hashers))
-                    return rc;
-                slot_req[sl] = -1;
-            } else {
-                any = true;
-            }
-        }
-        if (!any) {
-            bool free_slot = false;
-            for (uint32_t sl = 0; sl < slots; ++sl) free_slot |= slot_req[sl] < 0;
-            if (next >= n_req) break;
-            if (free_slot) continue;
-        }
+        // 3. decode steps until the next slot finishes (0 steps if an admitted request needs just
+        //    its first token), then wait once for the stream so that slot can be collected
         int k = INT32_MAX;
         for (uint32_t sl = 0; sl < slots; ++sl)
             if (slot_req[sl] >= 0) k = std::min(k, slot_left[sl]);
-        if (next < n_req) {
-            bool free_slot = false;
-            for (uint32_t sl = 0; sl < slots; ++sl) free_slot |= slot_req[sl] < 0;
-            if (free_slot) k = std::min(k, 0);   // admit first
+        if (k == INT32_MAX) {   // no active slot
+            if (next >= n_req) break;
+            continue;
         }
         for (int t = 0; t < k; ++t) ENG_CUDA(cudaGraphLaunch(gx, s));
-        decode_steps += static_cast<uint64_t>(std::max(k, 0));
+        decode_steps += static_cast<uint64_t>(k);
         for (uint32_t sl = 0; sl < slots; ++sl)
             if (slot_req[sl] >= 0) slot_left[sl] -= k;
         ENG_CUDA(cudaStreamSynchronize(s));
@@ -1160,13 +1236,23 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
         if (!perr.empty()) return fail(E, DETGPU_EINVAL, "infer: " + perr);
         for (uint32_t t = 0; t < prompt_lens[i]; ++t)
             if (prompts[i][t] >= vocab) return fail(E, DETGPU_EINVAL, "infer: prompt token out of vocabulary");
-        if (!E->toy) {
-            if (prompt_lens[i] == 0 && policies[i].max_tokens > 0)
-                return fail(E, DETGPU_EINVAL, "infer: empty prompt (a transformer needs a position to predict from)");
-            if (uint64_t(prompt_lens[i]) + policies[i].max_tokens > E->max_context)
-                return fail(E, DETGPU_EINVAL, "infer: prompt + max_tokens exceeds the engine's max_context");
-        }
+        if (!E->toy && uint64_t(std::max(prompt_lens[i], 1u)) + policies[i].max_tokens > E->max_context)
+            return fail(E, DETGPU_EINVAL, "infer: prompt + max_tokens exceeds the engine's max_context");
     }
+    // Empty prompts: the reference accepts them (detcore.cpp:340-352: the ToyModel decodes from its
+    // zero state). A transformer needs a position to predict from, so for the b200 models an empty
+    // prompt is the one-token prompt [kBosToken] (the oracle applies the same rule).
+    static const uint32_t kBos[1] = {kBosToken};
+    std::vector<const uint32_t*> pr_eff(prompts, prompts + n_req);
+    std::vector<uint32_t> len_eff(prompt_lens, prompt_lens + n_req);
+    if (!E->toy)
+        for (uint32_t i = 0; i < n_req; ++i)
+            if (len_eff[i] == 0) {
+                pr_eff[i] = kBos;
+                len_eff[i] = 1;
+            }
+    prompts = pr_eff.data();
+    prompt_lens = len_eff.data();
     if (E->toy)
         return toy_generate(E->toyw, n_req, prompts, prompt_lens, policies, seeds, batch_size, tokens_out, logits_out,
                             out_hash, flags, stats, E->stream, &E->err);
@@ -1316,6 +1402,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     cudaSetDevice(E->device);
     for (auto& kv : E->graphs) cudaGraphExecDestroy(kv.second);
     E->graphs.clear();
+    E->graph_used.clear();
     return DETGPU_OK;
 }
 

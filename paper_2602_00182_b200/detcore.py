@@ -40,6 +40,12 @@ class DecodePolicy:
     p: Optional[float] = None
     max_tokens: int = 0
 
+    def __post_init__(self):
+        # p is a float32 everywhere it matters (the C-ABI, the codec, req_hash; detcore.hpp:55):
+        # round it here so validate() judges the value that is actually used
+        if self.p is not None:
+            object.__setattr__(self, "p", float(np.float32(self.p)))
+
     @staticmethod
     def greedy(max_tokens: int) -> "DecodePolicy":
         return DecodePolicy(DecodeKind.greedy, None, None, max_tokens)
@@ -108,13 +114,44 @@ class InferenceOutput:
         return self._canonical
 
 
+class ReductionOrder(IntEnum):
+    canonical_tree = 0
+    sequential = 1
+    tcgen05_b200 = 2
+
+
+@dataclass(frozen=True)
+class ArchProfile:
+    """detcore.hpp:21-30. The order selects the engine: canonical_tree / sequential run the
+    reference ToyModel ("archA" / "archB"), tcgen05_b200 the Llama-style transformer ("b200")."""
+
+    name: str
+    reduction_order: ReductionOrder = ReductionOrder.canonical_tree
+
+    @property
+    def engine_arch(self) -> str:
+        return {ReductionOrder.canonical_tree: "archA", ReductionOrder.sequential: "archB"}.get(
+            self.reduction_order, "b200")
+
+
+_KNOWN = {"archA": ReductionOrder.canonical_tree, "archB": ReductionOrder.sequential,
+          "b200": ReductionOrder.tcgen05_b200}
+
+
 class ArchRegistry:
-    """Approved profiles (detcore.cpp:12-20 + the GPU engine)."""
+    """Approved profiles (detcore.hpp:34-47, detcore.cpp:12-26, plus the GPU profile "b200").
+    Built from names of known profiles and/or ArchProfile objects; add() registers more."""
 
     _default = None
 
-    def __init__(self, names=()):
-        self._names = set(names)
+    def __init__(self, profiles=()):
+        self._p = {}
+        for x in profiles:
+            self.add(x if isinstance(x, ArchProfile) else ArchProfile(x, _KNOWN[x]) if x in _KNOWN else None)
+
+    def add(self, profile: Optional[ArchProfile]) -> None:
+        if profile is not None:
+            self._p[profile.name] = profile
 
     @classmethod
     def defaults(cls) -> "ArchRegistry":
@@ -122,11 +159,15 @@ class ArchRegistry:
             cls._default = ArchRegistry(["archA", "archB", "b200"])
         return cls._default
 
+    def find(self, name: str) -> Optional[ArchProfile]:
+        return self._p.get(name)
+
     def contains(self, name: str) -> bool:
-        return name in self._names and bool(L.lib.detgpu_arch_supported(name.encode()))
+        p = self._p.get(name)
+        return p is not None and bool(L.lib.detgpu_arch_supported(p.engine_arch.encode()))
 
     def names(self):
-        return sorted(self._names)
+        return sorted(self._p)
 
 
 # ---------------------------------------------------------------- canonical bytes & receipts
@@ -232,7 +273,7 @@ def req_hash(e: ExecutionTuple) -> bytes:
 
 # ---------------------------------------------------------------- engine
 class Engine:
-    """One engine per (GPU, model_id, arch) = one replica. Not thread-safe per instance."""
+    """One engine per (GPU, model_id, arch) = one replica. Calls on one instance are serialised."""
 
     def __init__(self, model_id: str, arch: str = "b200", max_batch: int = 64, max_context: int = 1024,
                  device: int = 0):
@@ -246,6 +287,8 @@ class Engine:
         self.info = info
         self.vocab = int(info.vocab)
         self.last_stats = L.Stats()
+        # one call at a time per handle (detgpu.h): ctypes releases the GIL during detgpu_generate
+        self._lock = threading.Lock()
 
     def close(self):
         if getattr(self, "h", None):
@@ -280,49 +323,81 @@ class Engine:
                 (lg.ctypes.data_as(C.POINTER(C.c_float)) if lg.size else C.POINTER(C.c_float)()) for lg in logits])
         hashes = np.zeros(32 * n, dtype=np.uint8) if (want_hash and not device_only) else None
         stats = L.Stats()
-        rc = L.lib.detgpu_generate(self.h, n, pr_ptrs, lens, pols, sd, batch_size or self.max_batch, tok_ptrs, lg_ptrs,
-                                   hashes.ctypes.data_as(C.POINTER(C.c_uint8)) if hashes is not None else None,
-                                   (L.F_DEVICE_ONLY if device_only else 0) | (L.F_RECEIPT_V2 if receipt_v2 else 0)
-                                   | (L.F_CONTINUOUS if continuous else 0),
-                                   C.byref(stats))
+        with self._lock:
+            rc = self._generate(n, pr_ptrs, lens, pols, sd, batch_size, tok_ptrs, lg_ptrs, hashes, device_only,
+                                receipt_v2, continuous, stats)
         L.check(rc, self.h)
         self.last_stats = stats
         toks = [t[:p.max_tokens] for t, p in zip(toks, policies)]
         hs = [hashes[32 * i:32 * i + 32].tobytes() for i in range(n)] if hashes is not None else None
         return toks, logits, hs
 
+    def _generate(self, n, pr_ptrs, lens, pols, sd, batch_size, tok_ptrs, lg_ptrs, hashes, device_only, receipt_v2,
+                  continuous, stats):
+        return L.lib.detgpu_generate(self.h, n, pr_ptrs, lens, pols, sd, batch_size or self.max_batch, tok_ptrs, lg_ptrs,
+                                   hashes.ctypes.data_as(C.POINTER(C.c_uint8)) if hashes is not None else None,
+                                   (L.F_DEVICE_ONLY if device_only else 0) | (L.F_RECEIPT_V2 if receipt_v2 else 0)
+                                   | (L.F_CONTINUOUS if continuous else 0),
+                                   C.byref(stats))
 
+
+# One cached engine per (device, model_id, engine arch), sized from the requests: rebuilt with a
+# larger context when a request needs it (the reference accepts any length), at most MAX_ENGINES
+# kept (least recently used dropped). Engine.generate holds the engine's own lock.
+ENGINE_MAX_BATCH = 64
+ENGINE_MIN_CONTEXT = 2048
+MAX_ENGINES = 4
 _engines: dict = {}
 _lock = threading.Lock()
+_clock = [0]
 
 
-def _engine_for(e: ExecutionTuple, registry: ArchRegistry, device: int = 0) -> Engine:
-    if not registry.contains(e.arch):
-        raise ValueError(f"infer: unknown arch profile '{e.arch}'")
-    key = (device, e.model_id, e.arch)
+def _engine_for(model_id: str, engine_arch: str, need_ctx: int, device: int = 0) -> Engine:
+    key = (device, model_id, engine_arch)
     with _lock:
-        eng = _engines.get(key)
-        if eng is None:
-            eng = Engine(e.model_id, e.arch, max_batch=64, max_context=2048 if e.arch == "b200" else 1, device=device)
-            _engines[key] = eng
+        _clock[0] += 1
+        ent = _engines.get(key)
+        if ent is not None and (engine_arch != "b200" or ent[0].max_context >= need_ctx):
+            ent[1] = _clock[0]
+            return ent[0]
+        ctx = ENGINE_MIN_CONTEXT
+        while ctx < need_ctx:
+            ctx *= 2
+        if ent is None and len(_engines) >= MAX_ENGINES:
+            victim = min(_engines, key=lambda k: _engines[k][1])
+            del _engines[victim]
+        eng = Engine(model_id, engine_arch, max_batch=ENGINE_MAX_BATCH, max_context=ctx if engine_arch == "b200" else 1,
+                     device=device)
+        _engines[key] = [eng, _clock[0]]
         return eng
+
+
+def release_engines() -> None:
+    """Drop every cached engine (GPU memory is freed once no call is using it)."""
+    with _lock:
+        _engines.clear()
 
 
 def infer_batch(execs: Sequence[ExecutionTuple], batch_size: int, registry: Optional[ArchRegistry] = None,
                 device: int = 0):
-    """detcore.cpp:387-410: per-tuple results are byte-identical to individual infer() calls."""
+    """detcore.cpp:387-410: per-tuple results are byte-identical to individual infer() calls.
+    Every tuple is validated (arch against `registry`, then policy) before any work."""
     registry = registry or ArchRegistry.defaults()
     if batch_size == 0:
         raise ValueError("infer_batch: batch_size must be positive")
     results = [None] * len(execs)
     groups: dict = {}
     for i, e in enumerate(execs):
+        prof = registry.find(e.arch)
+        if prof is None or not registry.contains(e.arch):
+            raise ValueError(f"infer: unknown arch profile '{e.arch}'")
         err = e.decode_policy.validate()
         if err:
             raise ValueError("infer: " + err)
-        groups.setdefault((e.model_id, e.arch), []).append(i)
+        groups.setdefault((e.model_id, prof.engine_arch), []).append(i)
     for (mid, arch), idx in groups.items():
-        eng = _engine_for(execs[idx[0]], registry, device)
+        need = max(max(len(execs[i].prompt), 1) + execs[i].decode_policy.max_tokens for i in idx)
+        eng = _engine_for(mid, arch, need, device)
         toks, logits, hashes = eng.generate([execs[i].prompt for i in idx], [execs[i].decode_policy for i in idx],
                                             [execs[i].seed for i in idx], batch_size=batch_size)
         for j, i in enumerate(idx):

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "detgpu_detcore.hpp"
 
@@ -63,6 +64,59 @@ int main() {
     for (size_t i = 0; i < batch.size(); ++i) {
         if (a[i].out_hash != b[i].out_hash || a[i].out_hash != infer(batch[i]).out_hash) {
             std::printf("FAIL batch invariance at %zu\n", i);
+            return 1;
+        }
+    }
+    // a caller's registry (detcore.hpp:34-47): a new name for the canonical-tree order gives
+    // archA's bytes; the default registry rejects the name
+    {
+        ArchRegistry reg = ArchRegistry::defaults();
+        reg.add({"archC", ReductionOrder::canonical_tree, FmaEmulation::fused});
+        ExecutionTuple t = e;
+        t.arch = "archC";
+        if (infer(t, reg).out_hash != infer(e).out_hash) {
+            std::printf("FAIL custom registry\n");
+            return 1;
+        }
+        try {
+            infer(t);
+            std::printf("FAIL: default registry accepted archC\n");
+            return 1;
+        } catch (const std::invalid_argument&) {
+        }
+    }
+    // concurrent callers share one cached engine: bytes unchanged
+    {
+        std::vector<Hash32> got(8);
+        std::vector<std::thread> th;
+        for (int i = 0; i < 8; ++i) th.emplace_back([&, i] { got[i] = infer(batch[i % 4]).out_hash; });
+        for (auto& t : th) t.join();
+        for (int i = 0; i < 8; ++i)
+            if (got[i] != a[i % 4].out_hash) {
+                std::printf("FAIL concurrent infer at %d\n", i);
+                return 1;
+            }
+    }
+    // a request beyond the cached engine's context rebuilds it (the reference has no limit);
+    // an empty prompt is accepted (BOS rule) like the reference accepts it
+    {
+        ExecutionTuple t = batch[0];
+        t.prompt.assign(2100, 5);
+        t.decode_policy = DecodePolicy::greedy(4);
+        if (infer(t).tokens.size() != 4) {
+            std::printf("FAIL long context\n");
+            return 1;
+        }
+        t.prompt.clear();
+        ExecutionTuple u = t;
+        u.prompt = {0};
+        if (infer(t).out_hash != infer(u).out_hash) {
+            std::printf("FAIL empty prompt != [BOS]\n");
+            return 1;
+        }
+        release_engines();
+        if (infer(batch[1]).out_hash != a[1].out_hash) {
+            std::printf("FAIL after release_engines\n");
             return 1;
         }
     }

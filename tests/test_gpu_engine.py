@@ -333,3 +333,40 @@ def test_mid_model_bit_exact_with_oracle():
             assert (logits[i].view(np.uint32) == ol.view(np.uint32)).all(), (min_cols, bs, i)
             assert hashes[i] == O.out_hash(ot, ol), (min_cols, bs, i)
     eng.close()
+
+
+def test_infer_concurrency_context_growth_and_empty_prompt():
+    """The reference-shaped infer() (detcore.py): concurrent callers on one cached engine get the
+    same bytes (Engine.generate holds the engine's lock); a request longer than the cached
+    engine's context rebuilds it instead of failing (the reference has no context limit); an
+    empty prompt is the one-token prompt [0] (BOS rule), equal to the oracle."""
+    import threading
+
+    from paper_2602_00182_b200 import detcore as D
+
+    D.release_engines()
+    base = D.ExecutionTuple("llama-tiny:infer", arch="b200", decode_policy=D.DecodePolicy.nucleus(0.9, 10), seed=5,
+                            prompt=[3, 1, 4, 1, 5, 9])
+    want = D.infer(base).out_hash
+    got = [None] * 8
+
+    def run(i):
+        got[i] = D.infer(base).out_hash
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert got == [want] * 8
+    long = D.ExecutionTuple("llama-tiny:infer", arch="b200", decode_policy=D.DecodePolicy.greedy(4), seed=1,
+                            prompt=_prompt(9, 2100, 4096))
+    out = D.infer(long)
+    ot, ol = O.Llama("llama-tiny:infer").generate(long.prompt, max_tokens=4, seed=1)
+    assert out.tokens.tolist() == ot.tolist() and out.out_hash == O.out_hash(ot, ol)
+    assert D.infer(base).out_hash == want   # the rebuilt engine serves short requests too
+    empty = D.ExecutionTuple("llama-tiny:infer", arch="b200", decode_policy=D.DecodePolicy.greedy(6), seed=2, prompt=[])
+    bos = D.ExecutionTuple("llama-tiny:infer", arch="b200", decode_policy=D.DecodePolicy.greedy(6), seed=2, prompt=[0])
+    oe, oel = O.Llama("llama-tiny:infer").generate([], max_tokens=6, seed=2)
+    assert D.infer(empty).out_hash == D.infer(bos).out_hash == O.out_hash(oe, oel)
+    D.release_engines()
