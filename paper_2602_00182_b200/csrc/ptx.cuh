@@ -3,6 +3,7 @@
 // audited (UTCHMMA / UTMALDG / LDTM) against this file.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 
 #include "trace.h"
@@ -45,12 +46,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Blocking wait on a phase parity. A watchdog traps after ~4 s so a protocol bug surfaces as a
 // launch error instead of a hung GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// The call site's file and line are printed first, so a trap names the barrier.
+static __device__ __noinline__ void mbar_watchdog_report(uint32_t bar, uint32_t parity, int tag, const char* file,
+                                                        int line) {
+    if ((threadIdx.x & 31) == 0 || tag >= 0)
+        printf("detgpu mbar watchdog: %s:%d smem 0x%x parity %u tag %d block (%d,%d,%d) thread %d\n", file, line, bar,
+               parity, tag, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = -1,
+                                          const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait(a, parity)) {
-        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+        if (globaltimer_ns() - t0 > 4000000000ull) {
+            mbar_watchdog_report(a, parity, tag, file, line);
+            __trap();
+        }
     }
 }
 

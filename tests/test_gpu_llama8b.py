@@ -120,3 +120,18 @@ def test_nucleus_thousand_replays_match_oracle(eng8b):
         toks, _, h = eng8b.generate([pr], [pol], [seed], batch_size=1, want_logits=False)
         assert h[0].hex() == c["out_hash"]
         assert toks[0].tolist() == c["tokens"]
+
+
+def test_decode_graph_stress_batch_transitions(eng8b):
+    """Regression for the streamed-attention ring's phase-parity ABA (fixed in round 2: a consumer
+    group waiting for a stage's second use while the first use was still in flight passed its
+    parity wait early and the ring deadlocked; the mbarrier watchdog trapped ~1 % of batch-256
+    sweeps). CUDA-graph decode steps at batch 1 / 8 / 64 / 256, 20 rounds: every launch succeeds."""
+    import ctypes as C
+
+    from paper_2602_00182_b200 import _lib as L
+
+    for _ in range(20):
+        for b in (1, 8, 64, 256):
+            ms = C.c_float()
+            L.check(L.lib.detgpu_profile_graph(eng8b.h, b, 640, 0, 10, C.byref(ms)), eng8b.h)
