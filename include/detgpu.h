@@ -148,6 +148,9 @@ int detgpu_profile_decode_step(detgpu_engine* h, uint32_t ncols, uint32_t ctx, u
  *   "fuse_max_cols" decode RMSNorm folded into the consuming GEMMs up to this many columns
  *                 (default and maximum 8; 0: separate RMSNorm kernels)
  *   "max_nsub"    GEMM tiles above 64 columns: at most 2 or 4 64-column sub-tiles per CTA
+ *   "gemm_persist" GEMMs above 64 columns as persistent clusters with double-buffered TMEM and a
+ *                 push combine (bit-identical; 1: K-segment count S <= 2 only, 2: every S;
+ *                 default 0: measured slower inside the decode / prefill pipeline)
  *   "gemm_pair"   GEMMs above 64 columns as CTA pairs (tcgen05 cta_group::2, 256 x 128 tiles;
  *                 bit-identical; default 0: measured no faster than two one-CTA tiles per SM)
  *   "self_pf_kb"  GEMM CTAs warm this many of their own weight k-blocks (16 KB each) beyond the

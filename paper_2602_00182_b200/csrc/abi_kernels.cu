@@ -52,7 +52,10 @@ int detgpu_k_gemm_split(const void* W, const void* X, float* Y, int n_out, int K
     p.out = Y;
     p.ld_out = ldy;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (ksplit >= 200) {   // test hook: 200 + S (0: the shape rule) selects the CTA-pair kernel above 64 columns
+    if (ksplit >= 300) {   // test hook: 300 + S (0: the shape rule) selects the persistent kernel above 64 columns
+        p.persist = 2;
+        ksplit -= 300;
+    } else if (ksplit >= 200) {   // test hook: 200 + S (0: the shape rule) selects the CTA-pair kernel above 64 columns
         p.pair = 1;
         ksplit -= 200;
     }

@@ -140,6 +140,10 @@ struct Engine {
     int self_pf_kb_cls[5] = {-1, 0, -1, 0, -1};
     int self_pf_kb = 4;   // GemmParams::self_pf_kb (tools/l2pf_scan.py: 4 beat 8 by ~1 % at batch 1 and 8)
     int gemm_pair = 0;    // GemmParams::pair: CTA-pair (cta_group::2) GEMMs above 64 columns
+    // GemmParams::persist: persistent double-buffered GEMMs above 64 columns. Bit-identical and
+    // faster standalone for S = 2, but slower inside the PDL pipeline (one CTA per SM: the next
+    // kernel cannot start streaming during the tail; tools/persist_ab.py), so off by default.
+    int gemm_persist = 0;
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
@@ -362,6 +366,7 @@ GemmParams gemm_base(const Engine* E, const void* w, int n_out, int k, int ncols
     p.self_pf_kb = E->self_pf_kb;
     p.max_nsub = E->max_nsub;
     p.pair = E->gemm_pair;
+    p.persist = E->gemm_persist;
     p.w_tiled = 1;   // engine weights are stored pre-tiled
     p.mma_wide = 1;  // one N = 64*sub-tiles MMA per K step: column bits identical (tools/wide_mma_check.py)
 
@@ -1382,6 +1387,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     }
     else if (std::strcmp(name, "max_nsub") == 0) E->max_nsub = static_cast<int>(value);
     else if (std::strcmp(name, "gemm_pair") == 0) E->gemm_pair = static_cast<int>(value);
+    else if (std::strcmp(name, "gemm_persist") == 0) E->gemm_persist = static_cast<int>(value);
     else if (std::strcmp(name, "prefill_blocks") == 0) E->prefill_blocks = value != 0;
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_sep_recv_max_cols") == 0) E->attn_sep_recv_max_cols = static_cast<int>(value);

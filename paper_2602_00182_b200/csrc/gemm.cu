@@ -9,6 +9,8 @@
 // per weight row; here the reduction order over K is fixed by the k-block loop below and never
 // split across CTAs.
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.h"
 #include "gemm.cuh"
@@ -388,6 +390,58 @@ __device__ void norm_b_setup(const GemmParams& p, uint8_t* bc, uint64_t* bready,
 // finalises column quads seg, seg + S_, ...; warp group wg takes every other round of QB_ quads.
 // Per element the reference tree over the S_ partials in segment order (local_tree_sum<8>, -0
 // padded: the padding adds are exact and compile away for a constant S_).
+// The S_ partials of one column quad (v[s], segment order) -> the reference tree per element ->
+// the fused epilogue of the quad's live columns.
+template <int S_>
+__device__ __forceinline__ void finish_quad(const GemmParams& p, const float4 (&v)[S_], int q, int nq, int ncols,
+                                            int m0, int rl, int col0, const QkvRow& qr, const int* s_cpos,
+                                            const int64_t* s_ckv, ExpTab tab) {
+    float sum[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        float t[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            t[s] = s >= S_ ? kNegZero : e == 0 ? v[s].x : e == 1 ? v[s].y : e == 2 ? v[s].z : v[s].w;
+        sum[e] = local_tree_sum<8>(t);
+    }
+    if (p.mode == kEpiAddF32) {   // residual add: the quad's four loads first
+        float res[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            res[e] = q < nq && q * 4 + e < ncols ? p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] : 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (q < nq && q * 4 + e < ncols)
+                p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] = __fadd_rn(res[e], sum[e]);
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int cl = q * 4 + e;
+        if (q >= nq || cl >= ncols) continue;   // warp-uniform
+        if (p.mode == kEpiStoreF32) {
+            if (s_ckv[cl] >= 0) p.out[s_ckv[cl] + m0 + rl] = sum[e];
+            continue;
+        }
+        if (p.mode == kEpiQkvRope) {
+            const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
+            epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
+            continue;
+        }
+        if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
+            epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
+            ++e;   // both columns done
+            continue;
+        }
+        epilogue_any(p, m0 + rl, col0 + cl, sum[e], tab);   // ss_out: <= 8 cols
+    }
+}
+
+// Many-column combine (cluster form): CTA `seg` finalises column quads seg, seg + S_, ... reading
+// every segment's partial tile over DSMEM; warp group wg takes every other round of QB_ quads.
+// Per element the reference tree over the S_ partials in segment order (local_tree_sum<8>, -0
+// padded: the padding adds are exact and compile away for a constant S_).
 template <int S_, int QB_>
 __device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbase, int seg, int wg, int nq, int ncols,
                                               int m0, int rl, int col0, const QkvRow& qr, const int* s_cpos,
@@ -404,51 +458,21 @@ __device__ __forceinline__ void combine_quads(const GemmParams& p, uint32_t pbas
                                  : make_float4(kNegZero, kNegZero, kNegZero, kNegZero);
         }
 #pragma unroll
-        for (int u = 0; u < QB_; ++u) {
-            const int q = q0 + u * S_;
-            float sum[4];
+        for (int u = 0; u < QB_; ++u)
+            finish_quad<S_>(p, v[u], q0 + u * S_, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab);
+    }
+}
+// Persistent form: the partials were pushed into this CTA's receive buffer R
+// [source segment][owned quad j][row] (quad q = seg + j * S_), so every read is local.
+template <int S_>
+__device__ __forceinline__ void combine_local(const GemmParams& p, const float4* R, int qmax, int seg, int nq, int ncols,
+                                              int m0, int rl, int col0, const QkvRow& qr, const int* s_cpos,
+                                              const int64_t* s_ckv, ExpTab tab) {
+    for (int j = 0, q = seg; q < nq; ++j, q += S_) {
+        float4 v[S_];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                float t[8];
-#pragma unroll
-                for (int s = 0; s < 8; ++s)
-                    t[s] = s >= S_ ? kNegZero
-                         : e == 0 ? v[u][s].x : e == 1 ? v[u][s].y : e == 2 ? v[u][s].z : v[u][s].w;
-                sum[e] = local_tree_sum<8>(t);
-            }
-            if (p.mode == kEpiAddF32) {   // residual add: the quad's four loads first
-                float res[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    res[e] = q < nq && q * 4 + e < ncols
-                                 ? p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] : 0.0f;
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (q < nq && q * 4 + e < ncols)
-                        p.out[static_cast<int64_t>(col0 + q * 4 + e) * p.ld_out + m0 + rl] = __fadd_rn(res[e], sum[e]);
-                continue;
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int cl = q * 4 + e;
-                if (q >= nq || cl >= ncols) continue;   // warp-uniform
-                if (p.mode == kEpiStoreF32) {
-                    if (s_ckv[cl] >= 0) p.out[s_ckv[cl] + m0 + rl] = sum[e];
-                    continue;
-                }
-                if (p.mode == kEpiQkvRope) {
-                    const float partner = __shfl_xor_sync(0xffffffffu, sum[e], 1);
-                    epilogue_qkv_col(p, qr, col0 + cl, s_cpos[cl], s_ckv[cl], sum[e], partner);
-                    continue;
-                }
-                if (p.mode == kEpiSwiglu && (e & 1) == 0 && cl + 1 < ncols) {
-                    epilogue_swiglu_pair(p, m0 + rl, col0 + cl, sum[e], sum[e + 1], tab);
-                    ++e;   // both columns done
-                    continue;
-                }
-                epilogue_any(p, m0 + rl, col0 + cl, sum[e], tab);   // ss_out: <= 8 cols
-            }
-        }
+        for (int s = 0; s < S_; ++s) v[s] = R[(s * qmax + j) * BM + rl];
+        finish_quad<S_>(p, v, q, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab);
     }
 }
 
@@ -762,6 +786,299 @@ __global__ void __launch_bounds__(256, Cfg<NSUB>::MIN_CTAS)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Many columns (> 64), persistent: a cluster of S CTAs (one per K-segment, one CTA per SM) walks
+// the (weight tile, 128-column group) units round robin, so the grid is one wave whatever the
+// shape. TMEM holds two 128-column accumulators: the MMA of unit i+1 runs while the epilogue
+// warps move unit i's partial to shared memory, combine the S partials of their columns over DSMEM
+// (the segment tree, combine_quads) and run the fused epilogue. Per unit and column the arithmetic
+// is exactly gemm_tc_kernel's (same K-segments, same chains, same tree), so bits are identical
+// (tests/test_gpu_gemm.py::test_persistent_gemm_bit_identical).
+//
+// Cross-CTA hand-offs are mbarriers, not cluster barriers (the producer and MMA warps never stop).
+// The combine is a push: each CTA sends every column quad of its partial straight into the owner
+// CTA's receive buffer (st.async, completing bytes on the owner's `recv` barrier), so the owner
+// reads all S partials of its quads from local shared memory (no DSMEM round trip):
+//   recv     : the S partials of this CTA's quads of the unit have landed
+//   rfree    : every CTA finished combining the unit (S remote arrivals) -> receive buffers reusable
+//   tfull[b] / tempty[b] : TMEM accumulator b complete / drained (MMA <-> epilogue)
+constexpr int kPN = 128;                                   // columns per unit (two 64-wide sub-tiles)
+constexpr int kPStages = 4;
+constexpr int kPStageBytes = A_BYTES + 2 * B_BYTES;        // 32 KB
+constexpr int kPRecvBytes = 36 * BM * 16;                  // max over S of S * ceil(32 / S) quads x 128 rows x 16 B
+constexpr int kPSmem = kPStages * kPStageBytes + kPRecvBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_persist_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                        const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kPStages * A_BYTES;
+    float4* R = reinterpret_cast<float4*>(sB + kPStages * 2 * B_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(R) + kPRecvBytes);
+    uint64_t* empty = full + kPStages;
+    uint64_t* tfull = empty + kPStages;    // [2]
+    uint64_t* tempty = tfull + 2;          // [2]
+    uint64_t* recv = tempty + 2;
+    uint64_t* rfree = recv + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(rfree + 1);
+    __shared__ int s_cpos[kPN];
+    __shared__ int64_t s_ckv[kPN];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = p.ksplit;
+    const int seg = static_cast<int>(cluster_ctarank());
+    const int cid = blockIdx.x / S, ncl = gridDim.x / S;
+    const int ntiles = p.n_out / BM, ncg = (p.ncols + kPN - 1) / kPN;
+    const int nunits = ntiles * ncg;
+    const int nkb_all = p.k / BK;
+    const int kb0 = seg * nkb_all / S, kb1 = (seg + 1) * nkb_all / S, nkb = kb1 - kb0;
+    const int qmax = (kPN / 4 + S - 1) / S;   // owned quads per CTA, at most
+    const uint64_t t_start = globaltimer_ns();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int i = 0; i < kPStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 1);
+        }
+        mbar_init(recv, 1);
+        mbar_init(rfree, S);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tslot, 2 * kPN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync_all();   // every CTA's barriers initialised before any remote arrive / push
+    const uint32_t tbase = *tslot;
+
+    auto unit_geom = [&](int u, int& tile, int& col0, int& ncols) {
+        tile = u / ncg;   // consecutive units: the column groups of one tile (weights read once from HBM)
+        col0 = (u % ncg) * kPN;
+        ncols = min(kPN, p.ncols - col0);
+    };
+    auto load_w = [&](void* dst, uint64_t* bar, int tile, int kb) {
+        if (p.w_tiled) tma_load_3d(dst, &tmW, bar, 0, 0, tile * nkb_all + kb, kEvictFirst);
+        else tma_load_3d(dst, &tmW, bar, 0, kb, tile * BM, kEvictFirst);
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int s = 0, ph = 0;
+            bool first = true;
+            for (int u = cid; u < nunits; u += ncl) {
+                int tile, col0, ncols;
+                unit_geom(u, tile, col0, ncols);
+                const int nb = (ncols + SUB_N - 1) / SUB_N;
+                const uint32_t tx = A_BYTES + nb * B_BYTES;
+                int i0 = 0;
+                if (first) {   // weights do not depend on the previous kernel: stream them before the PDL wait
+                    const int pre = min(kPStages, nkb);
+                    for (int i = 0; i < pre; ++i) {
+                        mbar_arrive_expect_tx(&full[i], tx);
+                        load_w(sA + i * A_BYTES, &full[i], tile, kb0 + i);
+                    }
+                    pdl_wait();
+                    pdl_trigger();
+                    for (int i = 0; i < pre; ++i)
+                        for (int j = 0; j < nb; ++j)
+                            tma_load_2d(sB + (i * 2 + j) * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, col0 + j * SUB_N,
+                                        kEvictLast);
+                    s = pre % kPStages;
+                    ph = (pre / kPStages) & 1;
+                    i0 = pre;
+                    first = false;
+                }
+                for (int i = i0; i < nkb; ++i) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], tx);
+                    load_w(sA + s * A_BYTES, &full[s], tile, kb0 + i);
+                    for (int j = 0; j < nb; ++j)
+                        tma_load_2d(sB + (s * 2 + j) * B_BYTES, &tmX, &full[s], (kb0 + i) * BK, col0 + j * SUB_N,
+                                    kEvictLast);
+                    if (++s == kPStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            if (first) {   // no unit for this cluster
+                pdl_wait();
+                pdl_trigger();
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int s = 0, ph = 0, it = 0;
+            for (int u = cid; u < nunits; u += ncl, ++it) {
+                int tile, col0, ncols;
+                unit_geom(u, tile, col0, ncols);
+                const int nb = (ncols + SUB_N - 1) / SUB_N;
+                const uint32_t idesc = umma_idesc_bf16(BM, nb * SUB_N);
+                const int b = it & 1, use = it >> 1;
+                if (use > 0) mbar_wait(&tempty[b], (use - 1) & 1);   // the epilogue drained this buffer
+                tc_fence_after();
+                const uint32_t d = tbase + b * kPN;
+                for (int i = 0; i < nkb; ++i) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+                    const uint32_t b_base = smem_u32(sB + s * 2 * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)   // one N = nb*64 instruction (bit-identical to per sub-tile)
+                        tc_mma_bf16(d, umma_desc_k128(a_base + k * 32), umma_desc_k128(b_base + k * 32), idesc,
+                                    (i | k) != 0 ? 1u : 0u);
+                    tc_commit(&empty[s]);
+                    if (++s == kPStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                tc_commit(&tfull[b]);
+            }
+        }
+    } else if (warp == 3 && lane == 0) {
+        l2_prefetch_slice(p.l2pf, p.l2pf_bytes, blockIdx.x, gridDim.x);
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue: TMEM -> push -> combine
+        const int ew = warp - 4, rl = ew * 32 + lane;
+        const ExpTab tab = exp_tab_lane();
+        const uint32_t rbase = smem_u32(R), recv_addr = smem_u32(recv);
+        int it = 0;
+        for (int u = cid; u < nunits; u += ncl, ++it) {
+            int tile, col0, ncols;
+            unit_geom(u, tile, col0, ncols);
+            const int nb = (ncols + SUB_N - 1) / SUB_N;
+            const int nq = (ncols + 3) >> 2;
+            const int m0 = tile * BM;
+            const int b = it & 1, use = it >> 1;
+            // this unit's per-column epilogue operands (read only by this CTA's epilogue warps)
+            if (p.mode == kEpiStoreF32)
+                for (int c = rl; c < ncols; c += 128) {
+                    int64_t off = static_cast<int64_t>(col0 + c) * p.ld_out;
+                    if (p.col_step != nullptr) {
+                        const int st = p.col_step[col0 + c];
+                        off = st < 0 ? -1
+                                     : static_cast<int64_t>(p.col_slot[col0 + c]) * p.slot_stride +
+                                           static_cast<int64_t>(st) * p.n_out;
+                    }
+                    s_ckv[c] = off;
+                }
+            if (p.mode == kEpiQkvRope)
+                for (int c = rl; c < ncols; c += 128) {
+                    const int pos = p.col_pos[col0 + c];
+                    s_cpos[c] = pos;
+                    s_ckv[c] = pos < 0 ? 0
+                                       : ((static_cast<int64_t>(p.block_table[static_cast<int64_t>(p.col_req[col0 + c]) *
+                                                                                   p.max_pages + pos / p.page]) * p.hkv) *
+                                              p.page + pos % p.page) * p.hd;
+                }
+            const QkvRow qr = p.mode == kEpiQkvRope ? qkv_row(p, m0 + rl) : QkvRow{};
+            mbar_wait(&tfull[b], use & 1);
+            tc_fence_after();
+            if (it > 0) mbar_wait_cluster(rfree, (it - 1) & 1);   // every receive buffer of the cluster is free
+            if (threadIdx.x == 128) {   // our quads' S partials: arrival + expected bytes
+                const int own = seg < nq ? (nq - 1 - seg) / S + 1 : 0;
+                mbar_arrive_expect_tx(recv, static_cast<uint32_t>(S * own * BM * 16));
+            }
+            for (int j = 0; j < nb; ++j) {
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + b * kPN + j * SUB_N + h * 32, r);
+                    tc_wait_ld();
+                    const int q0 = (j * SUB_N + h * 32) >> 2;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int q = q0 + c;
+                        if (q >= nq) break;   // warp-uniform
+                        const uint32_t o = static_cast<uint32_t>(q % S);
+                        const uint32_t off = 16u * static_cast<uint32_t>((seg * qmax + q / S) * BM + rl);
+                        st_async_v4(mapa_shared(rbase + off, o), r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3],
+                                    mapa_shared(recv_addr, o));
+                    }
+                }
+            }
+            tc_fence_before();
+            epi_bar();
+            if (threadIdx.x == 128) mbar_arrive(&tempty[b]);   // the accumulator may be reused (unit it + 2)
+            mbar_wait_cluster(recv, it & 1);                   // all S partials of our quads landed
+            switch (S) {
+                case 2: combine_local<2>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 3: combine_local<3>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 4: combine_local<4>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 5: combine_local<5>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 6: combine_local<6>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                case 7: combine_local<7>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+                default: combine_local<8>(p, R, qmax, seg, nq, ncols, m0, rl, col0, qr, s_cpos, s_ckv, tab); break;
+            }
+            epi_bar();   // every epilogue thread's reads of R are complete
+            if (threadIdx.x == 128)
+                for (int r = 0; r < S; ++r) mbar_arrive_remote(mapa_shared(smem_u32(rfree), static_cast<uint32_t>(r)));
+        }
+    }
+    // nobody leaves while a peer may still push into it (every push lands before its owner's last recv wait)
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tbase, 2 * kPN);
+    }
+    if (p.trace != nullptr && threadIdx.x == 0) {
+        uint64_t marks[kTraceMarks] = {};
+        marks[0] = t_start;
+        trace_record(p.trace, (p.trace_tag << 24) | blockIdx.x, marks);
+    }
+}
+
+cudaError_t launch_persist(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p, cudaStream_t stream,
+                           bool pdl) {
+    static std::atomic<uint64_t> attr_devs{0};
+    int dev = 0;
+    if (attrs_needed(attr_devs, &dev)) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem);
+        if (e != cudaSuccess) return e;
+        attrs_done(attr_devs, dev);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = kPSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = p.ksplit;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    // as many clusters as are co-resident (clusters live inside one GPC: S = 5 or 8 leaves SMs idle),
+    // never more than there are units
+    static int max_clusters[9][64] = {};
+    int& mc = max_clusters[p.ksplit][dev & 63];
+    if (mc == 0) {
+        cfg.gridDim = dim3(p.ksplit * 148, 1, 1);
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, gemm_persist_kernel, &cfg) != cudaSuccess || n <= 0) return cudaErrorInvalidConfiguration;
+        mc = n;
+        if (std::getenv("DETGPU_DEBUG_PERSIST")) std::fprintf(stderr, "gemm_persist: S=%d -> %d clusters\n", p.ksplit, n);
+    }
+    const int nunits = (p.n_out / BM) * ((p.ncols + kPN - 1) / kPN);
+    cfg.gridDim = dim3(p.ksplit * (mc < nunits ? mc : nunits), 1, 1);
+    return cudaLaunchKernelEx(&cfg, gemm_persist_kernel, tmW, tmX, p);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Many columns (> 64): CTA pairs (cta_group::2). A pair computes a 256-row x 128-column tile of one
 // K-segment chain: each CTA loads its 128 weight rows and 64 of the 128 activation columns per
 // k-block (24 KB instead of 32 KB for the same 128 x 128 x 64 MACs per SM, four stages in flight
@@ -1064,6 +1381,11 @@ cudaError_t gemm_launch(const CUtensorMap& tmW, const CUtensorMap& tmX, const Ge
     if (p.ss_out != nullptr && (p.mode != kEpiAddF32 || p.n_out != p.ss_tiles * BM || p.ncols > 8))
         return cudaErrorInvalidValue;
     if (p.ncols <= 64) return launch_nsub<1>(tmW, tmX, p, stream, pdl);
+    // persistent clusters: faster for S = 2 (gate/up, lm_head: long K-segments keep the main loop
+    // busy while the push combine runs); at S = 5 / 8 the per-unit combine is longer than the main
+    // loop of 8-13 k-blocks and the one-unit clusters (two CTAs per SM) win (tools/gemm_persist_bench.py)
+    if (p.persist > 0 && p.ksplit > 1 && (p.ksplit <= 2 || p.persist > 1) && p.norm_x == nullptr && p.ss_out == nullptr)
+        return launch_persist(tmW, tmX, p, stream, pdl);
     // > 128 columns: 128-column tiles at two CTAs per SM (one CTA's epilogue overlaps the other's
     // main loop) beat 256-column tiles at one CTA per SM by 25 % on the 512-token prefill
     if (p.pair > 0 && p.n_out % (2 * BM) == 0 && 2 * p.ksplit <= 16 && p.norm_x == nullptr && p.ss_out == nullptr)

@@ -63,6 +63,7 @@ struct GemmParams {
     const void* w_raw;         // tiled weights (w_tiled): base pointer for the L2 self-prefetch below
     int max_nsub;              // > 128 columns: widest tile in 64-column sub-tiles (4, or 0: 2)
     int pair;                  // > 64 columns: CTA-pair tiles (gemm_pair_kernel, cta_group::2) when 1
+    int persist;               // > 64 columns: persistent clusters, double-buffered TMEM (gemm_persist_kernel)
     int self_pf_kb;            // before the PDL wait, warm up to this many of the CTA's own weight
                                // k-blocks beyond the shared-memory ring into L2 (0: off)
     const void* l2pf;          // optional: bytes warmed into L2 at kernel start (the next kernel's weights)

@@ -130,3 +130,25 @@ def test_cta_pair_gemm_bit_identical():
         check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y2.data_ptr(), n_out, K, ncols, n_out, 200 + S, None))
         torch.cuda.synchronize()
         assert torch.equal(Y1.view(torch.int32), Y2.view(torch.int32)), (n_out, K, ncols, S)
+
+
+def test_persistent_gemm_bit_identical():
+    """The persistent many-column form (gemm_persist_kernel: clusters of S CTAs walking (tile, 128-
+    column) units with double-buffered TMEM accumulators and mbarrier hand-offs over DSMEM) against
+    the one-unit-per-cluster form: every output bit equal, S = 2..8, ragged column counts, several
+    units per cluster (the accumulator buffers and the partial tile reused)."""
+    import torch
+    from paper_2602_00182_b200._lib import lib, check
+
+    g = torch.Generator().manual_seed(9)
+    for n_out, K, ncols, S in [(256, 512, 65, 2), (512, 1024, 200, 2), (2048, 1024, 1000, 2), (768, 2048, 300, 5),
+                               (4096, 4096, 512, 8), (1024, 1024, 129, 3), (6144, 4096, 256, 5), (4096, 14336, 384, 8),
+                               (28672, 4096, 130, 2)]:
+        W = _rand_bf16((n_out, K), g, 0.05)
+        X = _rand_bf16((ncols, K), g)
+        Y1 = torch.full((ncols, n_out), float("nan"), device="cuda")
+        Y2 = Y1.clone()
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y1.data_ptr(), n_out, K, ncols, n_out, S, None))
+        check(lib.detgpu_k_gemm_split(W.data_ptr(), X.data_ptr(), Y2.data_ptr(), n_out, K, ncols, n_out, 300 + S, None))
+        torch.cuda.synchronize()
+        assert torch.equal(Y1.view(torch.int32), Y2.view(torch.int32)), (n_out, K, ncols, S)
