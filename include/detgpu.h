@@ -170,6 +170,10 @@ int detgpu_trace_read(detgpu_engine* h, void* out, uint32_t max_records, uint32_
 int detgpu_profile_graph(detgpu_engine* h, uint32_t ncols, uint32_t ctx, uint32_t skip_mask, uint32_t reps,
                          float* ms_per_step);
 
+/* Out-of-bounds-write check (compute-sanitizer substitute): every engine device buffer is followed
+ * by a 4 KiB canary; counts the live buffers and those whose canary changed. */
+int detgpu_debug_check_canaries(uint64_t* n_checked, uint64_t* n_bad);
+
 /* ---- host-side helpers of the receipt path (no GPU needed) ---- */
 
 /* SHA-256 (receipts.hpp:53-54 hash_commit; sha256.cpp:32-37). */

@@ -51,6 +51,7 @@ def _load() -> C.CDLL:
     vp, sz, u32, i32, i64, u64 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_int, C.c_int64, C.c_uint64
     sig = {
         "detgpu_version": (C.c_char_p, []),
+        "detgpu_debug_check_canaries": (i32, [C.POINTER(u64), C.POINTER(u64)]),
         "detgpu_global_error": (C.c_char_p, []),
         "detgpu_arch_supported": (i32, [C.c_char_p]),
         "detgpu_create": (i32, [i32, C.c_char_p, C.c_char_p, u32, u32, C.POINTER(vp)]),

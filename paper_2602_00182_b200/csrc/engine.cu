@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <future>
@@ -34,9 +35,38 @@ namespace {
 constexpr int kPage = 64;          // KV positions per page
 constexpr int kPrefillCols = 2048; // max activation columns per forward pass
 
+// Every engine buffer is followed by a canary region (kCanaryBytes of 0xA5). compute-sanitizer is
+// not available on the GPU pool, so detgpu_debug_check_canaries() is the out-of-bounds-write
+// check the tests run after their workloads (tests/test_gpu_engine.py, tools/sanitize_run.py).
+constexpr size_t kCanaryBytes = 4096;
+struct CanaryReg {
+    std::mutex mu;
+    std::map<void*, std::pair<size_t, int>> live;   // base -> (payload bytes, device)
+};
+CanaryReg& canaries() {
+    static CanaryReg r;
+    return r;
+}
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
-    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(count, 1));
+    const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes + kCanaryBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(reinterpret_cast<uint8_t*>(*p) + bytes, 0xA5, kCanaryBytes);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(canaries().mu);
+    canaries().live[*p] = {bytes, dev};
+    return cudaSuccess;
+}
+void dfree(void* p) {
+    if (p == nullptr) return;
+    {
+        std::lock_guard<std::mutex> lk(canaries().mu);
+        canaries().live.erase(p);
+    }
+    cudaFree(p);
 }
 
 struct Layer {
@@ -162,16 +192,16 @@ struct Engine {
     ~Engine() {
         cudaSetDevice(device);
         for (auto& g : graphs) cudaGraphExecDestroy(g.second);
-        for (void* p : allocs) cudaFree(p);
-        if (trace) cudaFree(trace);
+        for (void* p : allocs) dfree(p);
+        if (trace) dfree(trace);
         if (trace_buf) cudaFree(trace_buf);
         for (auto& hb : hash_bufs) {
             if (hb.busy.valid()) hb.busy.wait();
             if (hb.p) cudaFreeHost(hb.p);
         }
-        if (tok_hist) cudaFree(tok_hist);
-        if (d_roots) cudaFree(d_roots);
-        if (d_steps) cudaFree(d_steps);
+        if (tok_hist) dfree(tok_hist);
+        if (d_roots) dfree(d_roots);
+        if (d_steps) dfree(d_steps);
         for (float* p : pinned)
             if (p) cudaFreeHost(p);
         for (auto e : ev)
@@ -612,7 +642,7 @@ int ensure_outputs(Engine* E, int nslots, int tmax) {
     tmax = tmax <= 64 ? (tmax <= 1 ? 1 : 1 << (32 - __builtin_clz(unsigned(tmax - 1)))) : (tmax + 63) / 64 * 64;
     const size_t need_trace = size_t(nslots) * tmax * E->cfg.V;
     if (need_trace > E->trace_cap) {
-        if (E->trace) cudaFree(E->trace);
+        if (E->trace) dfree(E->trace);
         E->trace = nullptr;
         ENG_CUDA(dalloc(&E->trace, need_trace));
         E->trace_cap = need_trace;
@@ -622,7 +652,7 @@ int ensure_outputs(Engine* E, int nslots, int tmax) {
     }
     const size_t need_tok = size_t(nslots) * tmax;
     if (need_tok > E->tok_cap) {
-        if (E->tok_hist) cudaFree(E->tok_hist);
+        if (E->tok_hist) dfree(E->tok_hist);
         E->tok_hist = nullptr;
         ENG_CUDA(dalloc(&E->tok_hist, need_tok));
         E->tok_cap = need_tok;
@@ -814,7 +844,7 @@ int collect_slot(Engine* E, int slot, uint32_t T, uint32_t* tokens_out, float* l
         if (T > 0) {
             const size_t need = 32 * size_t(T);
             if (need > E->roots_cap) {
-                if (E->d_roots) cudaFree(E->d_roots);
+                if (E->d_roots) dfree(E->d_roots);
                 E->d_roots = nullptr;
                 ENG_CUDA(dalloc(&E->d_roots, std::max(need, size_t(E->max_batch) * E->tcap * 32)));
                 E->roots_cap = std::max(need, size_t(E->max_batch) * E->tcap * 32);
@@ -1306,6 +1336,33 @@ int detgpu_generate(detgpu_engine* h, uint32_t n_req, const uint32_t* const* pro
 extern "C" {
 
 void* detgpu_stream(const detgpu_engine* h) { return h ? static_cast<void*>(h->e->stream) : nullptr; }
+
+int detgpu_debug_check_canaries(uint64_t* n_checked, uint64_t* n_bad) {
+    std::vector<std::pair<void*, std::pair<size_t, int>>> bufs;
+    {
+        std::lock_guard<std::mutex> lk(canaries().mu);
+        bufs.assign(canaries().live.begin(), canaries().live.end());
+    }
+    std::vector<uint8_t> host(kCanaryBytes);
+    uint64_t bad = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& b : bufs) {
+        cudaSetDevice(b.second.second);
+        if (cudaMemcpy(host.data(), static_cast<uint8_t*>(b.first) + b.second.first, kCanaryBytes,
+                       cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(nullptr, DETGPU_ECUDA, "check_canaries: cudaMemcpy failed");
+        for (uint8_t v : host)
+            if (v != 0xA5) {
+                ++bad;
+                break;
+            }
+    }
+    cudaSetDevice(cur);
+    if (n_checked) *n_checked = bufs.size();
+    if (n_bad) *n_bad = bad;
+    return DETGPU_OK;
+}
 
 // One decode forward + lm_head + sample for `ncols` slots at context `ctx`, launched without graph
 // or PDL, with a CUDA event after every launch on the engine stream. ms_by_class[k] is the mean

@@ -370,3 +370,27 @@ def test_infer_concurrency_context_growth_and_empty_prompt():
     oe, oel = O.Llama("llama-tiny:infer").generate([], max_tokens=6, seed=2)
     assert D.infer(empty).out_hash == D.infer(bos).out_hash == O.out_hash(oe, oel)
     D.release_engines()
+
+
+def test_no_out_of_bounds_writes_canaries():
+    """compute-sanitizer is closed on the GPU pool: every engine buffer carries a 4 KiB canary
+    (detgpu_debug_check_canaries). The sanitizer workload (tools/sanitize_run.py: cluster and
+    streamed attention, push / pull GEMM combines, the 32-CTA sampler with every policy,
+    continuous batching, the >16-chunk workspace combine) runs bit-exact with the oracle and leaves
+    every canary intact."""
+    import ctypes as C
+    import importlib.util
+
+    from paper_2602_00182_b200 import _lib as L
+
+    spec = importlib.util.spec_from_file_location("sanitize_run", Path(__file__).resolve().parents[1] / "tools" /
+                                                  "sanitize_run.py")
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    m.part_tiny(keep=True)
+    m.part_cont(keep=True)
+    m.part_mid(keep=True)
+    n, bad = C.c_uint64(), C.c_uint64()
+    L.check(L.lib.detgpu_debug_check_canaries(C.byref(n), C.byref(bad)))
+    assert n.value > 20 and bad.value == 0, (n.value, bad.value)
+    m.close_all()

@@ -1,8 +1,9 @@
-"""Workload for compute-sanitizer (racecheck / synccheck / memcheck): small engines that drive every
-hand-synchronised kernel path once, checked against the CPU oracle at the end so a run that
-"passes" the sanitizer also produced the right bytes.
+"""Checker workload: small engines that drive every hand-synchronised kernel path once, checked
+against the CPU oracle, then the out-of-bounds-write canaries of every engine buffer
+(detgpu_debug_check_canaries). compute-sanitizer is closed on the GPU pool (it left GPUs needing a
+reset); this is the substitute, run by tests/test_gpu_engine.py::test_no_out_of_bounds_writes_canaries.
 
-  compute-sanitizer --tool racecheck python tools/sanitize_run.py [--part all|tiny|mid|cont]
+  python tools/sanitize_run.py [--part all|tiny|mid|cont]
 
 Paths covered:
   * tcgen05 GEMM, decode push-combine (st.async into the owner's receive buffer) and prefill
@@ -44,7 +45,16 @@ def check(eng, orc, prompts, pols, seeds, **kw):
     return hashes
 
 
-def part_tiny():
+_KEEP = []
+
+
+def close_all():
+    for e in _KEEP:
+        e.close()
+    _KEEP.clear()
+
+
+def part_tiny(keep=False):
     eng = Engine("llama-tiny:san", "b200", max_batch=16, max_context=320)
     orc = O.Llama("llama-tiny:san")
     V = eng.vocab
@@ -57,10 +67,10 @@ def part_tiny():
     n = 12
     pr = [_prompt(20 + i, 3 + (i * 23) % 140, V) for i in range(n)]
     check(eng, orc, pr, [pols[i % 3] for i in range(n)], list(range(100, 100 + n)))
-    eng.close()
+    _KEEP.append(eng) if keep else eng.close()
 
 
-def part_cont():
+def part_cont(keep=False):
     eng = Engine("llama-tiny:san", "b200", max_batch=4, max_context=256)
     orc = O.Llama("llama-tiny:san")
     V = eng.vocab
@@ -68,17 +78,17 @@ def part_cont():
     pr = [_prompt(40 + i, 4 + 17 * i, V) for i in range(n)]
     pols = [DecodePolicy.greedy(2 + (i * 3) % 5) for i in range(n)]
     check(eng, orc, pr, pols, list(range(n)), batch_size=4, continuous=True)
-    eng.close()
+    _KEEP.append(eng) if keep else eng.close()
 
 
-def part_mid():
+def part_mid(keep=False):
     eng = Engine("llama-mid:san", "b200", max_batch=2, max_context=1200)
     orc = O.Llama("llama-mid:san")
     V = eng.vocab
     # 1,100-token context: > 16 chunks -> workspace + ticket combine in decode attention; prefill
     # on the many-column GEMM / query-block attention paths
     check(eng, orc, [_prompt(5, 1100, V)], [DecodePolicy.greedy(2)], [3])
-    eng.close()
+    _KEEP.append(eng) if keep else eng.close()
 
 
 def main():
@@ -86,11 +96,19 @@ def main():
     ap.add_argument("--part", default="all", choices=["all", "tiny", "mid", "cont"])
     a = ap.parse_args()
     parts = {"tiny": part_tiny, "cont": part_cont, "mid": part_mid}
+    import ctypes as C
+
+    from paper_2602_00182_b200 import _lib as L
+
     for name, fn in parts.items():
         if a.part in ("all", name):
             t0 = time.time()
-            fn()
+            fn(keep=True)
             print(f"sanitize_run part {name}: ok, bytes equal the oracle ({time.time() - t0:.0f} s)", flush=True)
+    n, bad = C.c_uint64(), C.c_uint64()
+    L.check(L.lib.detgpu_debug_check_canaries(C.byref(n), C.byref(bad)))
+    print(f"canaries: {n.value} buffers checked, {bad.value} overwritten", flush=True)
+    close_all()
 
 
 if __name__ == "__main__":
