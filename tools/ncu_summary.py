@@ -27,6 +27,9 @@ FULL_METRICS = [
 ]
 
 
+EXCLUDE = {"init_kernel"}
+
+
 def launches(path, out):
     rows = list(csv.reader(open(path)))
     hdr = None
@@ -42,11 +45,13 @@ def launches(path, out):
     scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}.get(unit, 1.0)
     for d in data:
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("detgpu::<unnamed>::", "").replace("unnamed>::", "")
+        if name in EXCLUDE:   # engine construction (weight generation), not part of the step
+            continue
         agg[name][0] += 1
         agg[name][1] += float(d["Metric Value"]) * scale
     tot = sum(v[1] for v in agg.values())
     lines = [f"# ncu launch list: {path}", "", "gpu__time_duration.sum per kernel (ncu, --clock-control none, "
-             "serialised and cold-cache: compare shares, not absolutes)", "",
+             "serialised and cold-cache: compare shares, not absolutes; engine weight initialisation excluded)", "",
              "| kernel | launches | total µs | share | mean µs |", "|---|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {100 * v[1] / tot:.1f}% | {v[1] / v[0]:.2f} |")
