@@ -50,26 +50,6 @@ struct Cfg {
     static constexpr int DPT = HD / kGT;                          // PV dimensions per thread
 };
 
-__device__ __forceinline__ void st_volatile_shared(int* p, int v) {
-    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_volatile_shared(const int* p) {
-    int v;
-    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-    return v;
-}
-// Spin until the producer has published chunk j into the stage (watchdog as mbar_wait's).
-__device__ __forceinline__ void wait_seq(const int* seq, int j) {
-    if (ld_volatile_shared(seq) == j) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (ld_volatile_shared(seq) != j) {
-        if (globaltimer_ns() - t0 > 4000000000ull) {
-            printf("detgpu seq watchdog: attn_stream chunk %d block %d thread %d\n", j, blockIdx.x, threadIdx.x);
-            __trap();
-        }
-    }
-}
-
 __device__ __forceinline__ void group_bar(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kGT) : "memory");
 }
@@ -115,7 +95,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* scr_all = ring + S * C::STAGE;
     __shared__ uint64_t full[S], empty[S];
     __shared__ int4 sinfo[S];
-    __shared__ int sseq[S];   // the chunk last published into each stage (see the consumer's wait)
     __shared__ int s_pos[kMaxCols], s_pref[kMaxCols + 1];
     __shared__ int s_last[kGroups];
     __shared__ int s_cnt[kLocalSlots];
@@ -127,7 +106,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid < S) {
         mbar_init(&full[tid], 1);
         mbar_init(&empty[tid], kGT);
-        sseq[tid] = -1;
     }
     if (tid == 0) fence_mbar_init();
     __syncthreads();
@@ -201,10 +179,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const __nv_bfloat16* src = a.q + static_cast<int64_t>(ci.col) * a.hq * HD + static_cast<int64_t>(ci.kvh) * G * HD;
             bulk_load(ring + s * C::STAGE + 2 * C::KB, src, C::QB, &full[s], kEvictLast);
         };
-        auto publish = [&](int s, int j, const ChunkInfo& ci) {
+        auto publish = [&](int s, const ChunkInfo& ci) {
             sinfo[s] = make_int4(ci.col, ci.kvh | (ci.c << 16), ci.n | (ci.nch << 16),
                                  ci.cnt | (ci.whole << 8) | (ci.key << 9));
-            st_volatile_shared(&sseq[s], j);
             mbar_arrive_expect_tx(&full[s], 2 * C::KB + C::QB);
         };
         // first fill: history chunks stream before the dependency wait (the QKV GEMM, our
@@ -215,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane < nfirst) {
             ci0 = locate(lane);
             pid0 = page_of(ci0);
-            publish(lane, lane, ci0);
+            publish(lane, ci0);
             if (ci0.c < ci0.nch - 1) issue_kv(lane, ci0, pid0);
         }
         pdl_wait();
@@ -236,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == i) {
                     const int j = jb + i, s = j % S;
                     mbar_wait(&empty[s], ((j / S) - 1) & 1, j);
-                    publish(s, j, ci);
+                    publish(s, ci);
                     issue_kv(s, ci, pid);
                     issue_q(s, ci);
                 }
@@ -262,11 +239,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = j % S;
         // Stage s is consumed by different groups on successive uses (S is not a multiple of the
         // group count), so this group has not itself waited for the stage's previous use j - S:
-        // while that phase is still in flight, a parity wait for chunk j would pass at once (the
-        // phase-parity ABA). Chunk j is published only after chunk j - S was consumed (its phase
-        // complete), so once sseq[s] == j the parity wait below is exact.
-        wait_seq(&sseq[s], j);
-        mbar_wait(&full[s], (j / S) & 1, gt == 0 ? j : -1);
+        // while that phase is still in flight, a parity wait for chunk j passes at once (the
+        // phase-parity ABA). First wait until chunk j - S has been released (empty[s] phase k - 1;
+        // exact: phase k - 2 is complete, since the producer published chunk j - S, and phase k is
+        // this group's own release of chunk j), after which full[s] is in phase k or k + 1 and the
+        // parity wait for chunk j is exact.
+        const int k = j / S;
+        if (k > 0) mbar_wait(&empty[s], (k - 1) & 1, gt == 0 ? j : -1);
+        mbar_wait(&full[s], k & 1, gt == 0 ? j : -1);
         const int4 inf = sinfo[s];
         const int col = inf.x, kvh = inf.y & 0xffff, c = inf.y >> 16, n = inf.z & 0xffff, nch = inf.z >> 16;
         const int lcnt = inf.w & 0xff, whole = (inf.w >> 8) & 1, key = inf.w >> 9;
