@@ -311,28 +311,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         group_bar(gi);
-        // PV: thread = DPT dimensions x G heads; fma chains over positions in order
+        // PV: thread = DPT dimensions x G heads; fma chains over positions in order. With two
+        // dimensions per thread the pair of chains of one head is one packed FFMA2 per position
+        // (each lane an independent fma.rn: the same bits as two scalar __fmaf_rn chains).
         float acc[G][DPT];
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int k = 0; k < DPT; ++k) acc[g][k] = 0.0f;
         {
             const int d0 = gt * DPT;
             const uint8_t* sV = st + C::KB;
             uint32_t voff[8];   // swizzled offset of (row r, d0) for r = p mod 8; rows 8 apart are 1 KB apart
 #pragma unroll
             for (int r = 0; r < 8; ++r) voff[r] = swz(r, d0);
-            auto pv_step = [&](int p, uint32_t off) {
-                float vv[DPT];
-                if constexpr (DPT == 2) {
-                    const uint32_t w = *reinterpret_cast<const uint32_t*>(sV + off);
-                    vv[0] = __uint_as_float(w << 16);
-                    vv[1] = __uint_as_float(w & 0xffff0000u);
-                } else {
-                    vv[0] = __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(sV + off)) << 16);
-                }
-                float ev[G];
+            auto load_e = [&](int p, float (&ev)[G]) {
                 if constexpr (G == 4) {
                     const float4 e4 = *reinterpret_cast<const float4*>(gE + p * 4);
                     ev[0] = e4.x;
@@ -343,17 +332,49 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int g = 0; g < G; ++g) ev[g] = gE[p * G + g];
                 }
+            };
+            if constexpr (DPT == 2) {
+                uint64_t acc2[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc2[g] = 0;
+                auto pv_step = [&](int p, uint32_t off) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(sV + off);
+                    const uint64_t vv = pack2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+                    float ev[G];
+                    load_e(p, ev);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc2[g] = ffma2(pack2(ev[g], ev[g]), vv, acc2[g]);
+                };
+                int p = 0;
+                for (; p + 8 <= n; p += 8) {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) pv_step(p + r, voff[r] + p * 128);
+                }
+                for (; p < n; ++p) pv_step(p, swz(p, d0));
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    acc[g][0] = lo32(acc2[g]);
+                    acc[g][1] = hi32(acc2[g]);
+                }
+            } else {
 #pragma unroll
                 for (int g = 0; g < G; ++g)
 #pragma unroll
-                    for (int k = 0; k < DPT; ++k) acc[g][k] = __fmaf_rn(ev[g], vv[k], acc[g][k]);
-            };
-            int p = 0;
-            for (; p + 8 <= n; p += 8) {
+                    for (int k = 0; k < DPT; ++k) acc[g][k] = 0.0f;
+                auto pv_step = [&](int p, uint32_t off) {
+                    const float v0 = __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(sV + off)) << 16);
+                    float ev[G];
+                    load_e(p, ev);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) pv_step(p + r, voff[r] + p * 128);
+                    for (int g = 0; g < G; ++g) acc[g][0] = __fmaf_rn(ev[g], v0, acc[g][0]);
+                };
+                int p = 0;
+                for (; p + 8 <= n; p += 8) {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) pv_step(p + r, voff[r] + p * 128);
+                }
+                for (; p < n; ++p) pv_step(p, swz(p, d0));
             }
-            for (; p < n; ++p) pv_step(p, swz(p, d0));
         }
         mbar_arrive(&empty[s]);   // this thread's reads of the stage are done
         __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
