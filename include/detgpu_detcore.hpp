@@ -135,8 +135,10 @@ struct Cache {
     std::map<std::tuple<int, std::string, std::string>, std::shared_ptr<CachedEngine>> engines;
 };
 inline Cache& cache() {
-    static Cache c;
-    return c;
+    // Never destroyed: engines still cached at process exit are reclaimed with the process. A
+    // static destructor would call detgpu_destroy after the CUDA runtime's own teardown has run.
+    static Cache* c = new Cache;
+    return *c;
 }
 inline const char* engine_arch(const ArchProfile& p) {
     switch (p.reduction_order) {

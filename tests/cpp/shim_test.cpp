@@ -20,6 +20,7 @@ static std::string hex(const uint8_t* p, size_t n) {
 }
 
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);   // a crash still shows how far it got
     ExecutionTuple e;
     e.model_id = "model-a";
     const char* c = "container-a";
@@ -128,5 +129,6 @@ int main() {
     } catch (const std::invalid_argument&) {
     }
     std::printf("OK\n");
+    std::fflush(stdout);
     return 0;
 }
