@@ -50,7 +50,10 @@ constexpr int kCombBar = 15;               // named barrier of the combiner warp
 // arithmetic is unchanged, so the split never changes a bit.
 template <int G>
 struct Split {
-    static constexpr int HS = G % 2 == 0 ? 2 : 1;
+#ifndef DETGPU_ATTN_HS
+#define DETGPU_ATTN_HS 1   // 2: measured slower (each half re-reads K and V: shared-memory traffic)
+#endif
+    static constexpr int HS = G % DETGPU_ATTN_HS == 0 ? DETGPU_ATTN_HS : 1;
     static constexpr int GH = G / HS;                        // query heads per consumer group
     static constexpr int NCG = kGroups * HS;                 // consumer groups
     static constexpr int PRODUCER_WARP = NCG * kGT / 32;
