@@ -42,9 +42,6 @@ constexpr int kMaxCols = 256;              // columns staged in shared memory
 constexpr int kMaxCombine = 64;            // chunks per (column, kv head): contexts up to 4096
 constexpr int kCopyBar = 14;               // named barrier of the copier warps
 constexpr int kCombBar = 15;               // named barrier of the combiner warps
-#ifndef DETGPU_ATTN_ABL
-#define DETGPU_ATTN_ABL 0   // timing ablations (A/B builds only, never the product)
-#endif
 // Head split: each chunk group is HS consumer groups of 64 threads, each owning G/HS of the kv
 // head's query heads for the whole chunk. The per-(head, position) and per-(head, dim)
 // arithmetic is unchanged, so the split never changes a bit.
@@ -312,8 +309,7 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
                 if (qs >= 2) mbar_wait(&qempty[qs & 1], ((qs >> 1) - 1) & 1, pt == 0 ? j : -1);
             }
             float* cb = cbuf + (qs & 1) * 2 * G * kMaxCombine;
-            if (DETGPU_ATTN_ABL == 8) {
-            } else if (nch == 1) {   // the combine weight is exp(0) == 1 exactly (as attn_chunk_kernel)
+            if (nch == 1) {   // the combine weight is exp(0) == 1 exactly (as attn_chunk_kernel)
                 __nv_bfloat16* outp = a.out + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
                 const float L = __fmaf_rn(ho[C::HO_ML / 4 + G + ph], 1.0f, 0.0f);
 #pragma unroll
@@ -360,7 +356,6 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
                     it.mode = s_last ? 2 : 0;
                 }
             }
-            if (DETGPU_ATTN_ABL == 3) it.mode = 0;
             // the copier threads' workspace stores are ordered before the combiner's reads: every
             // copier thread fences (CTA scope) and the queue entry is published after the barrier
             __threadfence_block();
