@@ -39,7 +39,7 @@ constexpr int kGT = 64;                    // threads per consumer group (two wa
 constexpr int kPT = 64;                    // copier threads (two warps)
 constexpr int kCT = 128;                   // combiner threads (four warps)
 constexpr int kMaxCols = 256;              // columns staged in shared memory
-constexpr int kMaxCombine = 64;            // chunks per (column, kv head): contexts up to 4096
+constexpr int kMaxCombine = 128;           // chunks per (column, kv head): contexts up to 8192
 constexpr int kCopyBar = 14;               // named barrier of the copier warps
 constexpr int kCombBar = 15;               // named barrier of the combiner warps
 // Head split: each chunk group is HS consumer groups of 64 threads, each owning G/HS of the kv

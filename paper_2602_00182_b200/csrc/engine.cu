@@ -177,7 +177,7 @@ struct Engine {
     int max_nsub = 0;     // GemmParams::max_nsub
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
-    int attn_stream_min_cols = 9;    // AttnParams::stream_min_cols (0: off)
+    int attn_stream_min_cols = 8;    // AttnParams::stream_min_cols (0: off); 8: batch 8 3.95 -> 3.86 ms, 5-7 slower (tools/l2pf_scan.py)
     int attn_sep_recv_max_cols = 2;   // AttnParams::sep_recv up to this many columns (0: never)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only

@@ -14,7 +14,7 @@ from paper_2602_00182_b200 import _lib as L  # noqa: E402
 from paper_2602_00182_b200.detcore import Engine  # noqa: E402
 
 DEFAULTS = {"l2pf_mask": 2, "l2pf_cap_mb": 16, "self_pf_kb": 4, "attn_cluster_max_cols": 8, "max_nsub": 0,
-            "attn_stream_min_cols": 9, "fuse_max_cols": 8, "attn_sep_recv_max_cols": 2, "self_pf_kb_qkv": -1,
+            "attn_stream_min_cols": 8, "fuse_max_cols": 8, "attn_sep_recv_max_cols": 2, "self_pf_kb_qkv": -1,
             "self_pf_kb_o": 0,
             "self_pf_kb_gate_up": -1, "self_pf_kb_down": 0, "self_pf_kb_lm_head": -1,
             "gemm_pair": 0}   # engine defaults
