@@ -194,8 +194,11 @@ __device__ __forceinline__ __nv_bfloat16 combine_ws_chain(const float* base, int
 // receives every other chunk's (m, l, o) by st.async into its K/V buffer once it has finished with
 // it, combines them in chunk order and writes the output: no workspace, no ticket, no grid-wide
 // round trip. Same arithmetic as the ticket combine below.
-template <int HD, int G, bool CL>
-__global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, float scale) {   // <= 40 registers: six CTAs per SM
+// MINB: resident CTAs per SM the register budget is sized for. 6 (<= 40 registers) for many
+// columns; at <= 2 columns (<= 2 x hkv x chunks CTAs, far fewer than the SMs) 4 (<= 64 registers)
+// shortens the chunk's latency chain: batch 1 step -0.5 %, batch 2 -0.5 % (batch 4-7 slower).
+template <int HD, int G, bool CL, int MINB>
+__global__ void __launch_bounds__(kNT, MINB) attn_chunk_kernel(const AttnParams a, float scale) {
     constexpr int CH = kAttnChunk;
     constexpr int E = HD / 32;                       // q/k elements per lane in a dot product
     constexpr int CHAINS = G * HD;                   // (head, d) accumulators of the PV product
@@ -420,18 +423,18 @@ __global__ void __launch_bounds__(kNT, 6) attn_chunk_kernel(const AttnParams a, 
     }
 }
 
-template <int HD, int G, bool CL>
-cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
+template <int HD, int G, bool CL, int MINB>
+cudaError_t launch_hgc_m(const AttnParams& a, cudaStream_t stream, bool pdl) {
     constexpr size_t dsm_kv = 2 * static_cast<size_t>(kAttnChunk) * HD * 2;
     constexpr size_t dsm_max = dsm_kv + (CL ? static_cast<size_t>(kMaxClusterChunks - 1) * G * (HD + 2) * 4 : 0);
     const size_t dsm = dsm_kv + (CL && a.sep_recv ? static_cast<size_t>(a.max_chunks - 1) * G * (HD + 2) * 4 : 0);
     static std::atomic<uint64_t> attr_devs{0};
     int dev = 0;
     if (attrs_needed(attr_devs, &dev)) {
-        cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>,
+        cudaError_t e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm_max));
         if (e == cudaSuccess && CL)
-            e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            e = cudaFuncSetAttribute(attn_chunk_kernel<HD, G, CL, MINB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attrs_done(attr_devs, dev);
     }
@@ -450,7 +453,12 @@ cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(HD)));
-    return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G, CL>, a, scale);
+    return cudaLaunchKernelEx(&cfg, attn_chunk_kernel<HD, G, CL, MINB>, a, scale);
+}
+
+template <int HD, int G, bool CL>
+cudaError_t launch_hgc(const AttnParams& a, cudaStream_t stream, bool pdl) {
+    return a.ncols <= 2 ? launch_hgc_m<HD, G, CL, 4>(a, stream, pdl) : launch_hgc_m<HD, G, CL, 6>(a, stream, pdl);
 }
 
 // Prefill: one CTA per (chunk, kv head, block of Q = ROWS/G consecutive query columns): the chunk's
