@@ -589,12 +589,14 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
             static_assert(2 * RPT == PR && kNT % TPR == 0, "PV mapping");
             const int d0 = (tid % TPR) * 2, r0 = (tid / TPR) * RPT;   // r0 warp-uniform
             const uint32_t* v32 = reinterpret_cast<const uint32_t*>(sV);
-            float acc[RPT][2];
+            // the two chains of a row are one packed FFMA2 per position (each lane an independent
+            // fma.rn: the same bits as two scalar __fmaf_rn chains)
+            uint64_t acc2[RPT];
             int nr[RPT];
             int nmin = CH;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
-                acc[k][0] = acc[k][1] = 0.0f;
+                acc2[k] = 0;
                 nr[k] = s_run[(r0 + k) / G];
                 nmin = min(nmin, nr[k]);
             }
@@ -602,23 +604,21 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
 #pragma unroll 4
             for (int p = 0; p < nmin; ++p) {   // every row active: no per-FMA guard
                 const uint32_t w = v32[(p * HD + d0) >> 1];
-                const float v0 = __uint_as_float(w << 16), v1 = __uint_as_float(w & 0xffff0000u);
+                const uint64_t vv = pack2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 #pragma unroll
                 for (int k = 0; k < RPT; ++k) {
                     const float e = srow[k * CH + p];
-                    acc[k][0] = __fmaf_rn(e, v0, acc[k][0]);
-                    acc[k][1] = __fmaf_rn(e, v1, acc[k][1]);
+                    acc2[k] = ffma2(pack2(e, e), vv, acc2[k]);
                 }
             }
             for (int p = nmin; p < nmax; ++p) {   // the causal edge
                 const uint32_t w = v32[(p * HD + d0) >> 1];
-                const float v0 = __uint_as_float(w << 16), v1 = __uint_as_float(w & 0xffff0000u);
+                const uint64_t vv = pack2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 #pragma unroll
                 for (int k = 0; k < RPT; ++k)
                     if (p < nr[k]) {
                         const float e = srow[k * CH + p];
-                        acc[k][0] = __fmaf_rn(e, v0, acc[k][0]);
-                        acc[k][1] = __fmaf_rn(e, v1, acc[k][1]);
+                        acc2[k] = ffma2(pack2(e, e), vv, acc2[k]);
                     }
             }
 #pragma unroll
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kNT, 4) attn_prefill_kernel(const AttnParams a
                 if (nr[k] == 0) continue;
                 float* ws = a.ws + ((static_cast<int64_t>(col0 + q) * a.hkv + kvh) * a.max_chunks + c) * G * (HD + 4) +
                             g * (HD + 4);
-                *reinterpret_cast<float2*>(ws + 4 + d0) = make_float2(acc[k][0], acc[k][1]);
+                *reinterpret_cast<float2*>(ws + 4 + d0) = make_float2(lo32(acc2[k]), hi32(acc2[k]));
                 if (d0 == 0) {
                     ws[0] = sM[r];
                     ws[1] = sL[r];
