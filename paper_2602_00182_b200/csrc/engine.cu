@@ -517,7 +517,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         }
         if (!(E->skip_mask & (1u << kProfO)) && (e = gemm_launch(Ly.tm_o, tm_attn, go, s, pdl)) != cudaSuccess) return e;
         mark(E, kProfO);
-        if (!fuse) {
+        if (!fuse && !(E->skip_mask & (1u << kProfNorm))) {
             if ((e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, Ly.ffn_norm, E->h, nullptr, ncols, d, c.eps, s,
                                     pdl)) != cudaSuccess)
                 return e;
@@ -561,6 +561,8 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         n += 6;
         if (fuse) {
             // norms fused into the next QKV GEMM / lm_head
+        } else if (l + 1 < c.L && (E->skip_mask & (1u << kProfNorm))) {
+            // timing experiments only: RMSNorm left out
         } else if (l + 1 < c.L) {
             e = launch_rmsnorm(E->x, nullptr, nullptr, nullptr, E->layers[l + 1].attn_norm, E->h, nullptr, ncols, d,
                                c.eps, s, pdl);

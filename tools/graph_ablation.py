@@ -11,7 +11,7 @@ from paper_2602_00182_b200.detcore import Engine  # noqa: E402
 QKV, ATTN, O, GU, DOWN = 1, 2, 3, 4, 5
 batch = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 eng = Engine("llama3-8b:bench", "b200", max_batch=max(batch, 1), max_context=768)
-cases = {"full": 0, "no_attn": 1 << ATTN, "no_qkv": 1 << QKV, "no_o": 1 << O, "no_gate_up": 1 << GU,
+cases = {"full": 0, "no_norm": 1, "no_attn": 1 << ATTN, "no_qkv": 1 << QKV, "no_o": 1 << O, "no_gate_up": 1 << GU,
          "no_down": 1 << DOWN, "only_gemm_gu_down": (1 << ATTN) | (1 << QKV) | (1 << O),
          "only_attn": (1 << QKV) | (1 << O) | (1 << GU) | (1 << DOWN), "nothing": (1 << ATTN) | (1 << QKV) | (1 << O) | (1 << GU) | (1 << DOWN)}
 out = {}
