@@ -372,12 +372,15 @@ __device__ __forceinline__ void sample_tail(const SampleParams& sp, SampleSmem& 
                         }
                         sm.kval = static_cast<uint64_t>(b);
                         sm.count = want - acc;
+                        sm.flag = sm.hist[b] == want - acc;   // the whole bin is taken: lower bits free
                     }
                     __syncthreads();
                     prefix |= sm.kval << shift;
                     mask |= 255ull << shift;
                     want = sm.count;
+                    const bool whole_bin = sm.flag != 0;
                     __syncthreads();
+                    if (whole_bin) break;   // every key with this prefix is >= kappa = prefix
                 }
                 kappa = prefix;
             }
