@@ -408,12 +408,12 @@ __device__ __forceinline__ void sample_tail(const SampleParams& sp, SampleSmem& 
                     __syncthreads();
                 }
             }
+            if (tid < take) sorted[consumed + tid] = sm.sort[tid];   // all threads: one store each
             if (tid == 0) {
                 int dec = 0;
                 for (int j = 0; j < take; ++j) {
                     const uint64_t k = sm.sort[j];
-                    sorted[consumed + j] = k;
-                    if (dec) continue;
+                    if (dec) break;
                     if (pol.kind == DETGPU_TOP_K) {
                         if (consumed + j + 1 >= target_k) {
                             kept = target_k;
@@ -442,20 +442,28 @@ __device__ __forceinline__ void sample_tail(const SampleParams& sp, SampleSmem& 
             consumed += take;
             __syncthreads();
         }
-        // renormalise with the canonical tree over the kept prefix, in sorted order
-        const float mass =
-            block_tree_sum_1024(kept, [&](int i, bool ok) { return ok ? key_prob(sorted[i]) : kNegZero; }, sm.tiles);
+        // renormalise with the canonical tree over the kept prefix, in sorted order. A prefix
+        // decided in the first round (consumed == 1024 or V) is still in shared memory.
+        const bool in_smem = consumed <= 1024;
+        auto kept_key = [&](int i) { return in_smem ? sm.sort[i] : sorted[i]; };
+        const float mass = block_tree_sum_1024(kept, [&](int i, bool ok) { return ok ? key_prob(kept_key(i)) : kNegZero; },
+                                               sm.tiles);
+        if (in_smem && mass > 0.0f) {   // the quotients p_i / mass in parallel (same divisions)
+            __syncthreads();            // sm.tiles is free again
+            if (tid < kept) sm.tiles[tid] = __fdiv_rn(key_prob(sm.sort[tid]), mass);
+            __syncthreads();
+        }
         if (tid == 0) {
             if (!(mass > 0.0f)) {
                 err = DETGPU_EINVAL;
                 token = 0;
             } else {
                 float c2 = 0.0f;
-                token = key_idx(sorted[kept - 1]);   // rounding left cum slightly below r
+                token = key_idx(kept_key(kept - 1));   // rounding left cum slightly below r
                 for (int i = 0; i < kept; ++i) {
-                    c2 = __fadd_rn(c2, __fdiv_rn(key_prob(sorted[i]), mass));
+                    c2 = __fadd_rn(c2, in_smem ? sm.tiles[i] : __fdiv_rn(key_prob(sorted[i]), mass));
                     if (c2 >= rdraw) {
-                        token = key_idx(sorted[i]);
+                        token = key_idx(kept_key(i));
                         break;
                     }
                 }
