@@ -247,16 +247,18 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
         const int nfirst = min(S, nloc);
         ChunkInfo ci0{};
         int pid0 = 0;
+        // (prefill: the predecessor writes every chunk's K/V of the prompt, so everything waits)
+        const bool early = a.decode != 0;
         if (lane < nfirst) {
             ci0 = locate(lane);
             pid0 = page_of(ci0);
             publish(lane, ci0);
-            if (ci0.c < ci0.nch - 1) issue_kv(lane, ci0, pid0);
+            if (early && ci0.c < ci0.nch - 1) issue_kv(lane, ci0, pid0);
         }
         pdl_wait();
         pdl_trigger();
         if (lane < nfirst) {
-            if (ci0.c == ci0.nch - 1) issue_kv(lane, ci0, pid0);
+            if (!early || ci0.c == ci0.nch - 1) issue_kv(lane, ci0, pid0);
             issue_q(lane, ci0);
         }
         for (int jb = S; jb < nloc; jb += 32) {
@@ -655,15 +657,34 @@ cudaError_t launch_stream_hg(const AttnParams& a, cudaStream_t stream, bool pdl)
 }  // namespace
 
 bool attention_stream_supported(const AttnParams& a) {
-    if (a.tm_k == nullptr || a.tm_v == nullptr || !a.decode) return false;
-    if (a.page != kAttnChunk || a.ncols > kMaxCols || a.max_chunks > kMaxCombine) return false;
+    if (a.tm_k == nullptr || a.tm_v == nullptr || (!a.decode && !a.stream_prefill)) return false;
+    if (a.page != kAttnChunk || (a.decode && a.ncols > kMaxCols) || a.max_chunks > kMaxCombine) return false;
     if (a.hkv <= 0 || a.hq % a.hkv != 0) return false;
     const int G = a.hq / a.hkv;
     return (a.hd == 128 && (G == 1 || G == 2 || G == 4)) || (a.hd == 64 && (G == 1 || G == 2 || G == 4));
 }
 
-cudaError_t launch_attention_stream(const AttnParams& a, cudaStream_t stream, bool pdl) {
-    if (!attention_stream_supported(a)) return cudaErrorInvalidValue;
+cudaError_t launch_attention_stream(const AttnParams& a_in, cudaStream_t stream, bool pdl) {
+    if (!attention_stream_supported(a_in)) return cudaErrorInvalidValue;
+    if (a_in.ncols > kMaxCols) {   // prefill chunks: consecutive launches of <= kMaxCols columns each
+        const int G = a_in.hq / a_in.hkv;
+        const int64_t cstride = static_cast<int64_t>(G) * (a_in.hd + 4);
+        for (int c0 = 0; c0 < a_in.ncols; c0 += kMaxCols) {
+            AttnParams a = a_in;
+            a.ncols = a_in.ncols - c0 < kMaxCols ? a_in.ncols - c0 : kMaxCols;
+            a.col_pos += c0;
+            a.col_req += c0;
+            a.q += static_cast<int64_t>(c0) * a.hq * a.hd;
+            a.out += static_cast<int64_t>(c0) * a.hq * a.hd;
+            a.ws += static_cast<int64_t>(c0) * a.hkv * a.max_chunks * cstride;
+            a.tickets += static_cast<int64_t>(c0) * a.hkv;
+            if (c0 > 0) a.l2pf_bytes = 0;
+            const cudaError_t e = launch_attention_stream(a, stream, pdl);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    const AttnParams& a = a_in;
     const int G = a.hq / a.hkv;
     if (a.hd == 128) {
         switch (G) {

@@ -178,6 +178,7 @@ struct Engine {
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
     int attn_stream_min_cols = 8;    // AttnParams::stream_min_cols (0: off); 8: batch 8 3.95 -> 3.86 ms, 5-7 slower (tools/l2pf_scan.py)
+    int attn_stream_prefill = 1;     // AttnParams::stream_prefill: 512-token prefill 18.45 -> 17.21 ms, 2,000 tokens 107.3 -> 98.7 ms
     int attn_sep_recv_max_cols = 2;   // AttnParams::sep_recv up to this many columns (0: never)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
     TraceRec* trace_buf = nullptr;   // per-CTA timeline (detgpu_set_option "trace"), instrumentation only
@@ -493,6 +494,7 @@ cudaError_t forward(Engine* E, int ncols, const int* tok, const int* pos, const 
         a.tm_v = &E->tm_vpool;
         a.kv_row0 = static_cast<int64_t>(per_layer / c.hd) * l;
         a.stream_min_cols = E->attn_stream_min_cols;
+        a.stream_prefill = E->attn_stream_prefill;
         a.trace = E->trace_buf;
         a.trace_tag = kProfAttn;
         if (pf & 1u) {
@@ -1451,6 +1453,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "attn_cluster_max_cols") == 0) E->attn_cluster_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_sep_recv_max_cols") == 0) E->attn_sep_recv_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_stream_min_cols") == 0) E->attn_stream_min_cols = static_cast<int>(value);
+    else if (std::strcmp(name, "attn_stream_prefill") == 0) E->attn_stream_prefill = static_cast<int>(value);
     else if (std::strcmp(name, "fuse_max_cols") == 0) E->fuse_max_cols = static_cast<int>(value < 0 ? 0 : value > 8 ? 8 : value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);

@@ -65,6 +65,7 @@ struct AttnParams {
     const CUtensorMap* tm_v;
     int64_t kv_row0;
     int stream_min_cols;
+    int stream_prefill;            // prefill chunks through the streamed kernel too (every K/V load after the wait)
 };
 size_t attn_workspace_bytes(const AttnParams& a);
 cudaError_t launch_attention(const AttnParams& a, cudaStream_t stream, bool pdl);

@@ -240,6 +240,33 @@ def test_streamed_decode_attention_bit_exact(tiny_oracle):
     eng.close()
 
 
+def test_prefill_through_streamed_attention_bit_exact(tiny_oracle):
+    """Prefill attention through the streamed kernel (option attn_stream_prefill: every K/V load after
+    the dependency wait, chunks of more than 256 prompt columns as consecutive launches) against the
+    query-block prefill kernel and the oracle: tiny model (hd 64) and llama-mid (hd 128, G 4),
+    several requests per prefill chunk, prompts of 1 to 900 tokens."""
+    from paper_2602_00182_b200.detcore import DecodePolicy, Engine
+
+    for model, lens in (("llama-tiny:model-a", [1, 63, 64, 65, 300, 511, 900, 17]),
+                        ("llama-mid:sp", [5, 129, 400, 70])):
+        eng = Engine(model, "b200", max_batch=len(lens), max_context=1024)
+        prompts = [_prompt(900 + i, n, eng.vocab) for i, n in enumerate(lens)]
+        pols = [DecodePolicy.greedy(3)] * len(lens)
+        seeds = list(range(len(lens)))
+        eng.set_option("attn_stream_prefill", 0)
+        ref_t, ref_l, ref_h = eng.generate(prompts, pols, seeds, batch_size=len(lens))
+        eng.set_option("attn_stream_prefill", 1)
+        t, l, h = eng.generate(prompts, pols, seeds, batch_size=len(lens))
+        assert h == ref_h, model
+        for i in range(len(lens)):
+            assert np.array_equal(l[i].view(np.uint32), ref_l[i].view(np.uint32)), (model, i)
+        if model.startswith("llama-tiny"):
+            ot, ol = tiny_oracle.generate(prompts[4], max_tokens=3, seed=seeds[4])
+            assert t[4].tolist() == ot.tolist()
+            assert (l[4].view(np.uint32) == ol.view(np.uint32)).all()
+        eng.close()
+
+
 def test_streamed_attention_items_spanning_many_ctas(tiny_oracle):
     """Few columns with long contexts: a (column, kv head) item's chunks spread over many persistent
     CTAs (global-ticket completion), and 32-chunk contexts; bit-identical to the cluster /

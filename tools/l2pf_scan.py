@@ -17,7 +17,7 @@ DEFAULTS = {"l2pf_mask": 2, "l2pf_cap_mb": 16, "self_pf_kb": 4, "attn_cluster_ma
             "attn_stream_min_cols": 8, "fuse_max_cols": 8, "attn_sep_recv_max_cols": 2, "self_pf_kb_qkv": -1,
             "self_pf_kb_o": 0,
             "self_pf_kb_gate_up": -1, "self_pf_kb_down": 0, "self_pf_kb_lm_head": -1,
-            "gemm_pair": 0}   # engine defaults
+            "gemm_pair": 0, "gemm_persist": 0, "attn_stream_prefill": 1}   # engine defaults
 ap = argparse.ArgumentParser()
 ap.add_argument("batch", nargs="?", type=int, default=1)
 ap.add_argument("ctx", nargs="?", type=int, default=640)
