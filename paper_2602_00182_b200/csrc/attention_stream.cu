@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
     // g0 .. g0 + GH - 1 of every chunk the chunk group takes
     const int cg = warp >> 1, gi = cg / HS, hh = cg % HS, gt = tid & (kGT - 1), wg = warp & 1;
     const int g0 = hh * GH;
-    float* gQ = reinterpret_cast<float*>(scr_all + cg * C::SCR);   // [GH][HD], {0,2,1,3}-permuted quads
+    float* gQ = reinterpret_cast<float*>(scr_all + cg * C::SCR);   // [GH][HD], 8-blocks as q0 q4 q1 q5 q2 q6 q3 q7 (qk_block8_x2)
     float* gS = gQ + GH * HD;                                       // [GH][64] scores
     float* gE = gS + GH * kCH;                                      // [64][GH] exp(s - m)
     float* gM = gE + kCH * GH;                                      // [GH] chunk max
@@ -480,13 +480,13 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
         const int n = inf.z & 0xffff;
         const uint8_t* st = ring + s * C::STAGE;
         const uint16_t* sq = reinterpret_cast<const uint16_t*>(st + 2 * C::KB) + g0 * HD;
-        for (int i = gt * 8; i < GH * HD; i += kGT * 8) {   // q -> f32; within each quad the order 0,2,1,3
+        for (int i = gt * 8; i < GH * HD; i += kGT * 8) {   // q -> f32, each 8-block as q0 q4 q1 q5 q2 q6 q3 q7
             const uint4 w = *reinterpret_cast<const uint4*>(sq + i);
-            *reinterpret_cast<float4*>(gQ + i) = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.y << 16),
+            *reinterpret_cast<float4*>(gQ + i) = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.z << 16),
                                                              __uint_as_float(w.x & 0xffff0000u),
-                                                             __uint_as_float(w.y & 0xffff0000u));
-            *reinterpret_cast<float4*>(gQ + i + 4) = make_float4(__uint_as_float(w.z << 16), __uint_as_float(w.w << 16),
-                                                                 __uint_as_float(w.z & 0xffff0000u),
+                                                             __uint_as_float(w.z & 0xffff0000u));
+            *reinterpret_cast<float4*>(gQ + i + 4) = make_float4(__uint_as_float(w.y << 16), __uint_as_float(w.w << 16),
+                                                                 __uint_as_float(w.y & 0xffff0000u),
                                                                  __uint_as_float(w.w & 0xffff0000u));
         }
         group_bar(cg);
@@ -500,8 +500,8 @@ __global__ void __launch_bounds__(Split<G>::THREADS, 1)
                 const uint4 kv = *reinterpret_cast<const uint4*>(st + kbase + (((v & 7) ^ (p & 7)) << 4) + (v >> 3) * (kCH * 128));
 #pragma unroll
                 for (int g = 0; g < GH; ++g) {
-                    float carry = qk_block8(kv, *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8),
-                                            *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8 + 4));
+                    float carry = qk_block8_x2(kv, *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8),
+                                               *reinterpret_cast<const ulonglong2*>(gQ + g * HD + v * 8 + 4));
                     int lvl = 0;
 #pragma unroll
                     for (int bb = v; bb & 1; bb >>= 1, ++lvl) carry = __fadd_rn(stk[g][lvl], carry);

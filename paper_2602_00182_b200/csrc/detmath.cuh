@@ -151,6 +151,24 @@ __device__ __forceinline__ float qk_block8(uint4 kv, ulonglong2 qa, ulonglong2 q
     const uint64_t s1 = fma2(qb.x, k46, mul2(qb.y, k57));   // {p4+p5, p6+p7}
     return __fadd_rn(__fadd_rn(lo32(s0), hi32(s0)), __fadd_rn(lo32(s1), hi32(s1)));
 }
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// The same canonical 8-product block with the second level packed too: q stored per 8-block as
+// q0 q4 q1 q5 | q2 q6 q3 q7 (qa, qb), so the level-1 pairs land as (p0+p1, p4+p5) and
+// (p2+p3, p6+p7) and one packed add forms (p0..3, p4..7). Same tree, same bits as qk_block8.
+__device__ __forceinline__ float qk_block8_x2(uint4 kv, ulonglong2 qa, ulonglong2 qb) {
+    const uint64_t k04 = (static_cast<uint64_t>(kv.z << 16) << 32) | (kv.x << 16);
+    const uint64_t k15 = (static_cast<uint64_t>(kv.z & 0xffff0000u) << 32) | (kv.x & 0xffff0000u);
+    const uint64_t k26 = (static_cast<uint64_t>(kv.w << 16) << 32) | (kv.y << 16);
+    const uint64_t k37 = (static_cast<uint64_t>(kv.w & 0xffff0000u) << 32) | (kv.y & 0xffff0000u);
+    const uint64_t sa = fma2(qa.x, k04, mul2(qa.y, k15));   // {p0+p1, p4+p5}
+    const uint64_t sb = fma2(qb.x, k26, mul2(qb.y, k37));   // {p2+p3, p6+p7}
+    const uint64_t t = add2(sa, sb);                         // {p0+..+p3, p4+..+p7}
+    return __fadd_rn(lo32(t), hi32(t));
+}
 // index of q element i in the permuted quad layout qk_block8 reads (swap 1 <-> 2 in each quad)
 __host__ __device__ constexpr int qperm(int i) { return (i & ~3) | ((i & 3) == 1 ? 2 : (i & 3) == 2 ? 1 : (i & 3)); }
 
