@@ -74,7 +74,7 @@ __device__ __forceinline__ void chunk_scores(const __nv_bfloat16* sK, const floa
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const uint4 kv = *reinterpret_cast<const uint4*>(sK + p * HD + ((v ^ (p & (NV - 1))) * 8));
-            float carry = qk_block8(kv, *reinterpret_cast<const ulonglong2*>(sQ + g * HD + v * 8),
+            float carry = qk_block8_x2(kv, *reinterpret_cast<const ulonglong2*>(sQ + g * HD + v * 8),
                                     *reinterpret_cast<const ulonglong2*>(sQ + g * HD + v * 8 + 4));
             int lvl = 0;
 #pragma unroll
@@ -293,14 +293,14 @@ __global__ void __launch_bounds__(kNT, MINB) attn_chunk_kernel(const AttnParams 
         load_rows(0, n);
     }
     cp_async_commit();
-    // q: 8 bf16 per 16-byte load (one L2 round trip), stored as f32 quads in qk_block8 order
+    // q: 8 bf16 per 16-byte load (one L2 round trip), stored as f32 in qk_block8_x2 order
     const __nv_bfloat16* qsrc = a.q + static_cast<int64_t>(col) * a.hq * HD + static_cast<int64_t>(kvh) * G * HD;
     for (int i = tid * 8; i < G * HD; i += kNT * 8) {
         const uint4 w = *reinterpret_cast<const uint4*>(qsrc + i);
-        *reinterpret_cast<float4*>(sQ + i) = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.y << 16),
-                                                         __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y & 0xffff0000u));
-        *reinterpret_cast<float4*>(sQ + i + 4) = make_float4(__uint_as_float(w.z << 16), __uint_as_float(w.w << 16),
-                                                             __uint_as_float(w.z & 0xffff0000u),
+        *reinterpret_cast<float4*>(sQ + i) = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.z << 16),
+                                                         __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.z & 0xffff0000u));
+        *reinterpret_cast<float4*>(sQ + i + 4) = make_float4(__uint_as_float(w.y << 16), __uint_as_float(w.w << 16),
+                                                             __uint_as_float(w.y & 0xffff0000u),
                                                              __uint_as_float(w.w & 0xffff0000u));
     }
     cp_async_wait_all();
