@@ -178,6 +178,7 @@ struct Engine {
     bool prefill_blocks = true;   // AttnParams::prefill_blocks
     int fuse_max_cols = 8;           // decode RMSNorm fused into the consuming GEMMs up to this many columns (<= 8)
     int attn_stream_min_cols = 8;    // AttnParams::stream_min_cols (0: off); 8: batch 8 3.95 -> 3.86 ms, 5-7 slower (tools/l2pf_scan.py)
+    bool mixed_steps = true;         // continuous batching: admitted prompts' last prefill chunk + one decode step in one forward
     int attn_stream_prefill = 1;     // AttnParams::stream_prefill: 512-token prefill 18.45 -> 17.21 ms, 2,000 tokens 107.3 -> 98.7 ms
     int attn_sep_recv_max_cols = 2;   // AttnParams::sep_recv up to this many columns (0: never)
     int attn_cluster_max_cols = 8;   // AttnParams::cluster_max_cols (crossover measured with tools/l2pf_scan.py)
@@ -1013,7 +1014,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         if (int rc = get_graph(E, static_cast<int>(slots), &gx)) return rc;
     std::vector<int> slot_req(slots, -1), slot_left(slots, 0);
     uint32_t next = 0;
-    uint64_t nl = 0, decode_steps = 0;
+    uint64_t nl = 0, decode_steps = 0, graph_steps = 0;
     Timer tall;
     double prefill_ms = 0;
     std::vector<int> ctok, cpos, creq, lin, lout, adm;
@@ -1055,10 +1056,86 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         }
         if (!adm.empty()) {
             Timer tp;
+            // Slots still decoding ride along: the last prefill chunk of the admitted prompts and one
+            // decode step of every decoding slot run as ONE forward pass (columns [0, slots) = the
+            // slots' decode columns, then the prompt columns), so the weights are streamed once for
+            // both. Columns are independent (batch invariance), so the bytes are unchanged.
+            std::vector<char> admitted(slots, 0);
+            for (int sl : adm) admitted[sl] = 1;
+            int ndec = 0;
+            for (uint32_t sl = 0; sl < slots; ++sl)
+                if (slot_req[sl] >= 0 && !admitted[sl] && slot_left[sl] > 0) ++ndec;
+            const bool mix = ndec > 0 && E->mixed_steps;
+            const int base = mix ? static_cast<int>(slots) : 0;
+            const int cap = E->col_cap - base;
+            auto flush = [&](bool last) -> int {
+                if (ctok.empty() && !(last && mix)) return DETGPU_OK;
+                const bool with_dec = last && mix;
+                const int nc = static_cast<int>(ctok.size());
+                if (with_dec)   // decoding slots: column sl -> h_last row sl
+                    for (uint32_t sl = 0; sl < slots; ++sl)
+                        if (slot_req[sl] >= 0 && !admitted[sl]) {
+                            lin.push_back(-1 - static_cast<int>(sl));   // marker: decode column sl
+                            lout.push_back(static_cast<int>(sl));
+                        }
+                const int nlast = static_cast<int>(lin.size());
+                const int off = with_dec ? base : 0;
+                void* bp = nullptr;
+                int bi = 0;
+                ENG_CUDA(stage_acquire(E, sizeof(int) * (3 * size_t(nc) + 2 * size_t(nlast)), &bp, &bi));
+                int* bb = static_cast<int*>(bp);
+                std::copy(ctok.begin(), ctok.end(), bb);
+                std::copy(cpos.begin(), cpos.end(), bb + nc);
+                std::copy(creq.begin(), creq.end(), bb + 2 * nc);
+                for (int i = 0; i < nlast; ++i)   // prompt lasts: chunk index -> column off + index
+                    bb[3 * nc + i] = lin[i] < 0 ? -1 - lin[i] : off + lin[i];
+                std::copy(lout.begin(), lout.end(), bb + 3 * nc + nlast);
+                if (with_dec) {   // the slots' decode state as the first `slots` columns
+                    ENG_CUDA(cudaMemcpyAsync(E->p_tok, E->d_tok, sizeof(int) * slots, cudaMemcpyDeviceToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_pos, E->d_pos, sizeof(int) * slots, cudaMemcpyDeviceToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_req, E->d_req, sizeof(int) * slots, cudaMemcpyDeviceToDevice, s));
+                }
+                if (nc > 0) {
+                    ENG_CUDA(cudaMemcpyAsync(E->p_tok + off, bb, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_pos + off, bb + nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_req + off, bb + 2 * nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
+                }
+                if (nlast > 0) {
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_in, bb + 3 * nc, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                    ENG_CUDA(cudaMemcpyAsync(E->p_last_out, bb + 3 * nc + nlast, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
+                }
+                ENG_CUDA(stage_release(E, bi));
+                if (st) st->h2d_bytes += sizeof(int) * (3ull * nc + 2ull * nlast) + sizeof(uint32_t) * nc;
+                ENG_CUDA(forward(E, off + nc, E->p_tok, E->p_pos, E->p_req, false, nlast, &nl));
+                ctok.clear();
+                cpos.clear();
+                creq.clear();
+                lin.clear();
+                lout.clear();
+                return DETGPU_OK;
+            };
+            for (size_t j = 0; j < adm.size(); ++j) {   // prompts as prefill columns; h_last[slot] = last position
+                const int r = slot_req[adm[j]];
+                for (uint32_t t = 0; t < lens[r]; ++t) {
+                    if (static_cast<int>(ctok.size()) == cap)
+                        if (int rc = flush(false)) return rc;
+                    if (t + 1 == lens[r]) {
+                        lin.push_back(static_cast<int>(ctok.size()));
+                        lout.push_back(adm[j]);
+                    }
+                    ctok.push_back(static_cast<int>(prompts[r][t]));
+                    cpos.push_back(static_cast<int>(t));
+                    creq.push_back(adm[j]);
+                }
+            }
+            if (int rc = flush(true)) return rc;
+            // the admitted slots' decode state (after the forward: their columns were not decode
+            // columns in it), then one sampler pass over the slots: the first token of each admitted
+            // request (trace step 0) and, when mixed, the next token of every decoding slot
             struct AdmState {   // the slot's decode state before its first token is sampled
                 uint64_t prng[4];
                 DevPolicy dp;
-                int pos, status;
+                int pos, status, step;
             };
             void* sp = nullptr;
             int si = 0;
@@ -1070,73 +1147,22 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
                 as[j].dp = to_dev_policy(pols[r]);
                 as[j].pos = static_cast<int>(lens[r]) - 1;
                 as[j].status = 0;
+                as[j].step = 0;
                 ENG_CUDA(cudaMemcpyAsync(E->d_prng + 4 * size_t(sl), as[j].prng, sizeof(as[j].prng), cudaMemcpyHostToDevice, s));
                 ENG_CUDA(cudaMemcpyAsync(E->d_pol + sl, &as[j].dp, sizeof(DevPolicy), cudaMemcpyHostToDevice, s));
                 ENG_CUDA(cudaMemcpyAsync(E->d_pos + sl, &as[j].pos, sizeof(int), cudaMemcpyHostToDevice, s));
                 ENG_CUDA(cudaMemcpyAsync(E->d_status + sl, &as[j].status, sizeof(int), cudaMemcpyHostToDevice, s));
-                if (st) st->h2d_bytes += sizeof(as[j].prng) + sizeof(DevPolicy) + 2 * sizeof(int);
+                ENG_CUDA(cudaMemcpyAsync(E->d_step + sl, &as[j].step, sizeof(int), cudaMemcpyHostToDevice, s));
+                if (st) st->h2d_bytes += sizeof(as[j].prng) + sizeof(DevPolicy) + 3 * sizeof(int);
             }
             ENG_CUDA(stage_release(E, si));
-            auto flush = [&]() -> int {
-                if (ctok.empty()) return DETGPU_OK;
-                const int nc = static_cast<int>(ctok.size());
-                const int nlast = static_cast<int>(lin.size());
-                void* bp = nullptr;
-                int bi = 0;
-                ENG_CUDA(stage_acquire(E, sizeof(int) * (3 * size_t(nc) + 2 * size_t(nlast)), &bp, &bi));
-                int* b = static_cast<int*>(bp);
-                std::copy(ctok.begin(), ctok.end(), b);
-                std::copy(cpos.begin(), cpos.end(), b + nc);
-                std::copy(creq.begin(), creq.end(), b + 2 * nc);
-                std::copy(lin.begin(), lin.end(), b + 3 * nc);
-                std::copy(lout.begin(), lout.end(), b + 3 * nc + nlast);
-                ENG_CUDA(cudaMemcpyAsync(E->p_tok, b, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->p_pos, b + nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
-                ENG_CUDA(cudaMemcpyAsync(E->p_req, b + 2 * nc, sizeof(int) * nc, cudaMemcpyHostToDevice, s));
-                if (nlast > 0) {
-                    ENG_CUDA(cudaMemcpyAsync(E->p_last_in, b + 3 * nc, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
-                    ENG_CUDA(cudaMemcpyAsync(E->p_last_out, b + 3 * nc + nlast, sizeof(int) * nlast, cudaMemcpyHostToDevice, s));
-                }
-                ENG_CUDA(stage_release(E, bi));
-                if (st) st->h2d_bytes += sizeof(int) * (3ull * nc + 2ull * nlast) + sizeof(uint32_t) * nc;
-                ENG_CUDA(forward(E, nc, E->p_tok, E->p_pos, E->p_req, false, nlast, &nl));
-                ctok.clear();
-                cpos.clear();
-                creq.clear();
-                lin.clear();
-                lout.clear();
-                return DETGPU_OK;
-            };
-            for (size_t j = 0; j < adm.size(); ++j) {   // prompts as prefill columns; h_last[j] = last position
-                const int r = slot_req[adm[j]];
-                for (uint32_t t = 0; t < lens[r]; ++t) {
-                    if (static_cast<int>(ctok.size()) == E->col_cap)
-                        if (int rc = flush()) return rc;
-                    if (t + 1 == lens[r]) {
-                        lin.push_back(static_cast<int>(ctok.size()));
-                        lout.push_back(static_cast<int>(j));
-                    }
-                    ctok.push_back(static_cast<int>(prompts[r][t]));
-                    cpos.push_back(static_cast<int>(t));
-                    creq.push_back(adm[j]);
-                }
-            }
-            if (int rc = flush()) return rc;
-            // first token of each admitted request: compact columns, trace step 0 of its slot
-            void* pp = nullptr;
-            int pi = 0;
-            ENG_CUDA(stage_acquire(E, 2 * sizeof(int) * adm.size(), &pp, &pi));
-            int* pb = static_cast<int*>(pp);
-            for (size_t j = 0; j < adm.size(); ++j) {
-                pb[j] = 0;
-                pb[adm.size() + j] = adm[j];
-            }
-            ENG_CUDA(cudaMemcpyAsync(E->p_last_in, pb, sizeof(int) * adm.size(), cudaMemcpyHostToDevice, s));
-            ENG_CUDA(cudaMemcpyAsync(E->p_last_out, pb + adm.size(), sizeof(int) * adm.size(), cudaMemcpyHostToDevice, s));
-            ENG_CUDA(stage_release(E, pi));
-            ENG_CUDA(head_and_sample(E, E->h_last, static_cast<int>(adm.size()), &nl, false, E->p_last_in,
-                                     E->p_last_out, true));
+            ENG_CUDA(head_and_sample(E, E->h_last, static_cast<int>(slots), &nl, false, E->d_step, E->d_req, false));
             for (int sl : adm) slot_left[sl] = static_cast<int>(pols[slot_req[sl]].max_tokens) - 1;
+            if (mix) {
+                for (uint32_t sl = 0; sl < slots; ++sl)
+                    if (slot_req[sl] >= 0 && !admitted[sl]) slot_left[sl] -= 1;
+                decode_steps += 1;
+            }
             prefill_ms += tp.ms();
         }
         // 3. decode steps until the next slot finishes (0 steps if an admitted request needs just
@@ -1150,6 +1176,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         }
         for (int t = 0; t < k; ++t) ENG_CUDA(cudaGraphLaunch(gx, s));
         decode_steps += static_cast<uint64_t>(k);
+        graph_steps += static_cast<uint64_t>(k);
         for (uint32_t sl = 0; sl < slots; ++sl)
             if (slot_req[sl] >= 0) slot_left[sl] -= k;
         ENG_CUDA(cudaStreamSynchronize(s));
@@ -1158,7 +1185,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
         st->prefill_ms += static_cast<float>(prefill_ms);
         st->decode_ms += static_cast<float>(tall.ms() - prefill_ms);
         st->decode_steps += decode_steps;
-        st->kernel_launches += nl + decode_steps * E->launches_per_step;
+        st->kernel_launches += nl + graph_steps * E->launches_per_step;
     }
     return DETGPU_OK;
 }
@@ -1454,6 +1481,7 @@ int detgpu_set_option(detgpu_engine* h, const char* name, int64_t value) {
     else if (std::strcmp(name, "attn_sep_recv_max_cols") == 0) E->attn_sep_recv_max_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_stream_min_cols") == 0) E->attn_stream_min_cols = static_cast<int>(value);
     else if (std::strcmp(name, "attn_stream_prefill") == 0) E->attn_stream_prefill = static_cast<int>(value);
+    else if (std::strcmp(name, "mixed_steps") == 0) E->mixed_steps = value != 0;
     else if (std::strcmp(name, "fuse_max_cols") == 0) E->fuse_max_cols = static_cast<int>(value < 0 ? 0 : value > 8 ? 8 : value);
     else if (std::strcmp(name, "trace") == 0) {
         cudaSetDevice(E->device);
