@@ -1065,7 +1065,7 @@ int run_continuous(Engine* E, uint32_t n_req, const uint32_t* const* prompts, co
             int ndec = 0;
             for (uint32_t sl = 0; sl < slots; ++sl)
                 if (slot_req[sl] >= 0 && !admitted[sl] && slot_left[sl] > 0) ++ndec;
-            const bool mix = ndec > 0 && E->mixed_steps;
+            const bool mix = ndec > 0 && E->mixed_steps && static_cast<int>(slots) + 64 <= E->col_cap;
             const int base = mix ? static_cast<int>(slots) : 0;
             const int cap = E->col_cap - base;
             auto flush = [&](bool last) -> int {
